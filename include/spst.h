@@ -1,0 +1,136 @@
+/* spst.h — C ABI of the B200-native SPST hot path (libspst.so).
+ *
+ * Replaces, for one device, the compute behind the reference's public Python entry points
+ * (paths relative to /root/reference/pkg/src/tilestyle/):
+ *   localized.py:162  stats_pass        -> spst_forward + spst_stats_ptrs + spst_finalize
+ *   localized.py:187  build_problem     -> spst_bind + spst_forward + spst_capture_content
+ *   localized.py:227  loss_grad         -> spst_forward, spst_finalize, spst_content_sqdiff,
+ *                                          spst_backward
+ *   localized.py:283  loss_grad_global  -> same calls with the whole image as one grid
+ *   lbfgs.py:68       two_loop_direction-> spst_vec_* step kernels (device scalars)
+ *   lbfgs.py:99       minimize          -> spst_vec_axpy / spst_vec_sy / spst_vec_absmax
+ *   tensorops.py:136  resize_down       -> spst_resize_down
+ *   tensorops.py:158  resize_bilinear   -> spst_resize_bilinear
+ * The reference has no FFI for this path (it is pure NumPy); the Python package
+ * paper_2212_13459_b200 binds these symbols with ctypes.
+ *
+ * Conventions: all pointers named *_dev are device pointers; images are HWC float32; status
+ * codes map 1:1 onto the reference's exception taxonomy (errors.py:4-33). No C++ exception
+ * crosses this boundary; spst_last_error() returns the message of the last failure.
+ * A context is bound to one device and one stream and is not thread-safe.
+ */
+#ifndef SPST_H_
+#define SPST_H_
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SPST_ABI_VERSION 1
+
+#define SPST_OK 0
+#define SPST_ERR_SHAPE 1       /* errors.ShapeError    */
+#define SPST_ERR_GEOMETRY 2    /* errors.GeometryError */
+#define SPST_ERR_CONFIG 3      /* errors.ConfigError   */
+#define SPST_ERR_NONFINITE 4   /* errors.NonFiniteError */
+#define SPST_ERR_CUDA 5        /* RuntimeError (CUDA failure) */
+#define SPST_ERR_OOM 6         /* MemoryError          */
+#define SPST_ERR_UNSUPPORTED 7 /* NotImplementedError: layer graph outside the device path */
+#define SPST_ERR_EMPTY 8       /* errors.EmptyError    */
+
+#define SPST_LAYER_CONV 0
+#define SPST_LAYER_RELU 1
+#define SPST_LAYER_AVGPOOL 2
+#define SPST_LAYER_MAXPOOL 3
+
+typedef struct spst_ctx spst_ctx;
+
+int spst_abi_version(void);
+const char* spst_status_string(int status);
+
+/* ---------------------------------------------------------------- extractor context ----
+ * extractor.py:72-106 ExtractorSpec + extractor.py:257-280 load_weights.
+ * layers: n_layers kinds (SPST_LAYER_*); conv layers carry cin/cout and float64 weights
+ * (cout, cin, 3, 3) + bias (cout); style_layers / content_layer are layer indices of relu
+ * layers; mean3/scale3/bgr is the Preprocess record (extractor.py:58-62). */
+int spst_create(int device, int n_layers, const int* kinds, const int* cin, const int* cout,
+                const double* const* weights, const double* const* biases, int n_style,
+                const int* style_layers, int content_layer, int bgr, const double* mean3,
+                const double* scale3, spst_ctx** out);
+void spst_destroy(spst_ctx* ctx);
+const char* spst_last_error(const spst_ctx* ctx);
+int spst_set_stream(spst_ctx* ctx, void* cuda_stream);
+
+/* Geometry (localized.py:116-120 make_grid, tiling.py:57-72). h, w: unpadded image. The
+ * padded grid is (Hp, Wp) = dims rounded up to the deepest stride. This context evaluates
+ * padded rows [grid_r0, grid_r1) as one zero-padded image and owns rows [own_r0, own_r1)
+ * (statistics, content loss and gradient are restricted to owned rows; the rows outside
+ * are the receptive-field halo). A single device binds grid = own = [0, Hp). */
+int spst_bind(spst_ctx* ctx, int h, int w, int grid_r0, int grid_r1, int own_r0, int own_r1);
+int spst_padded_dims(const spst_ctx* ctx, int* Hp, int* Wp);
+int spst_tap_info(const spst_ctx* ctx, int tap, int* channels, int* stride, long long* owned_pixels);
+long long spst_workspace_bytes(const spst_ctx* ctx);
+
+/* Forward pass of image x_dev (h x w x 3 f32). flags bit0: keep the state the backward needs.
+ * Leaves per style tap the owned-row partial sums S = sum F F^T (C x C f64) and s = sum F
+ * (C f64) in device buffers exposed by spst_stats_ptrs (for an NCCL all-reduce). */
+int spst_forward(spst_ctx* ctx, const float* x_dev, int flags);
+int spst_stats_ptrs(spst_ctx* ctx, int tap, double** S_dev, double** s_dev);
+
+/* Content target (localized.py:205-212): copy the content-tap features of the last forward. */
+int spst_capture_content(spst_ctx* ctx);
+/* sum over owned rows of (V - V_u)^2 at the content tap, into out_dev (1 f64). */
+int spst_content_sqdiff(spst_ctx* ctx, double* out_dev);
+
+/* Style reference of tap t (stats.py:22-31 LayerStats) and its TapWeights (stats.py:81-86). */
+int spst_set_style_ref(spst_ctx* ctx, int tap, const double* gram, const double* mean,
+                       const double* std, double w_gram, double w_mean, double w_std);
+/* Finalize global statistics from the (all-reduced) sums with global pixel counts n[tap]
+ * (stats.py:59-66), write per tap the three weighted loss terms (stats.py:117-124) to
+ * terms_host[3*tap..], and prepare the closed-form feature gradients (stats.py:127-165).
+ * degenerate_host[tap] = 1 when a zero-std channel has a nonzero reference std. */
+int spst_finalize(spst_ctx* ctx, const long long* n, double* terms_host, int* degenerate_host);
+/* Reverse pass (extractor.py:200-214 + localized.py:246-279): pixel gradient of the loss on
+ * owned rows written into grad_dev (h x w x 3 f32; rows outside the owned range untouched).
+ * two_lambda = 2 * lambda_c (0 disables the content term). */
+int spst_backward(spst_ctx* ctx, double two_lambda, float* grad_dev);
+
+/* ---------------------------------------------------------------- vector kernels ---------
+ * lbfgs.py:68-142. Reductions accumulate in f64 with a fixed order (deterministic). The
+ * partial buffer must hold spst_vec_partials() doubles per reduced quantity. */
+int spst_vec_partials(void);
+int spst_vec_dots(const float* a0, const float* b0, const float* a1, const float* b1,
+                  const float* a2, const float* b2, long long n, double* partial_dev,
+                  double* out_dev, void* stream);
+int spst_vec_absmax(const float* a, long long n, float* partial_dev, float* out_dev, void* stream);
+/* q_out = cscale * (q_in + coef_dev[0] * v); partial <w, q_out> (w may be NULL). */
+int spst_vec_axpy_dot(const float* q_in, float* q_out, const float* v, const double* coef_dev,
+                      double cscale, const float* w, long long n, double* partial_dev, void* stream);
+/* mode 0: alpha_dev = rho*sum(partial), coef_dev = -alpha; mode 1: coef = alpha - rho*sum */
+int spst_vec_twoloop_scalar(const double* partial_dev, double rho, int mode, double* alpha_dev,
+                            double* coef_dev, void* stream);
+int spst_vec_sum_partials(const double* partial_dev, int n_quantities, double* out_dev, void* stream);
+int spst_vec_axpy(const float* x, const float* d, float t, long long n, float* out, void* stream);
+int spst_vec_sy(const float* xt, const float* x, const float* gt, const float* g, long long n,
+                float* s, float* y, double* partial_dev, double* out_dev /*[3]: ys, ss, yy*/,
+                void* stream);
+
+/* ---------------------------------------------------------------- resampling ------------ */
+int spst_resize_down(const float* in, int h, int w, int c, int factor, float* out, void* stream);
+int spst_resize_bilinear(const float* in, int h, int w, int c, int oh, int ow, float* out,
+                         void* stream);
+
+/* ---------------------------------------------------------------- unit-test hooks -------
+ * One tensor-core conv layer on host arrays (x: cin x H x W f32, weight cout x cin x 3 x 3,
+ * bias cout; f64). mode 0: y = relu(conv(x)) (cout x H x W); mode 1: y = avgpool(relu(conv))
+ * (cout x H/2 x W/2); mode 2: y = conv^T(x) input gradient (x has cout channels, y cin);
+ * mode 3: relu mask bits of mode 0 as floats. Returns through y_host. */
+int spst_debug_conv(int device, int mode, int cin, int cout, int H, int W, const float* x_host,
+                    const double* weight, const double* bias, float* y_host);
+/* Gram of a (C x P) f32 feature matrix through the tensor-core Gram kernel, S = F F^T (f64). */
+int spst_debug_gram(int device, int C, long long P, const float* f_host, double* S_host);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPST_H_ */

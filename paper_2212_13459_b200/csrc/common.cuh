@@ -1,0 +1,162 @@
+// common.cuh — shared host/device definitions of the SPST device runtime.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cuda_fp16.h>
+
+namespace spst {
+
+constexpr int kSMs = 148;
+
+// Activation storage ("HL16"): fp16 hi plane-set followed by fp16 lo plane-set, each laid out
+// [C_p/8][H][W][8] (8 channels = 16 B per pixel per kgroup).  The stored value is x * 2^e,
+// split so that hi + lo carries ~22 mantissa bits.  Mask storage: uint32 [C_p/32][H][W],
+// bit j of word g = (pre-activation of channel 32g+j > 0).
+struct HL16 {
+  __half* hi = nullptr;   // lo = hi + planes * H * W * 8
+  int C_p = 0, H = 0, W = 0;
+  float scale = 1.f;      // 2^e
+  __host__ __device__ size_t plane_elems() const { return (size_t)H * W * 8; }
+  __host__ __device__ __half* lo() const { return hi + (size_t)(C_p / 8) * plane_elems(); }
+  __host__ __device__ size_t bytes() const { return (size_t)C_p * H * W * 4; }
+};
+
+enum EpiKind : int {
+  EPI_FWD = 0,        // relu(acc*s + bias) -> mask bits, full-res store (optional), channel sums
+  EPI_FWD_POOL = 1,   // as EPI_FWD plus 2x2 average pool of the two tile rows
+  EPI_BWD = 2,        // (acc*s + bvec + content + addend) * mask -> store
+  EPI_BWD_POOL = 3,   // pool adjoint: spread (acc*s)/4 onto 2x2 hi-res pixels (+addend) * hi-res mask
+};
+
+// Parameters of one tcgen05 3x3 implicit-GEMM launch (forward or input-gradient).
+struct ConvArgs {
+  CUtensorMap tm_a_hi, tm_a_lo;  // K operand: input activations (box 8 x 130 x 4 x 2)
+  CUtensorMap tm_v_hi, tm_v_lo;  // extra-K operand: tap features at the output pixels
+  const uint8_t* wgt;            // [ntile][kc][pass][tap][kg][n][8] fp16
+  const uint8_t* xwgt;           // [ntile][xkc][pass][kg][n][8] fp16 (extra K, one tap)
+  int H, W;                      // output (== input) spatial dims of the GEMM grid
+  int n_kc, n_xkc;               // conv K-chunks (16 ch each), extra K-chunks
+  int n_ntiles;                  // output channel tiles
+  int tiles_x, tiles_y;          // 128-px column blocks, 2-row row blocks
+  float acc_scale;               // 2^-(e_in + f)
+  float out_scale;               // 2^e_out
+  int epi;
+  // epilogue operands
+  const float* bias;             // [C_out_p] (fwd bias or bwd bvec), may be null
+  const uint32_t* mask_in;       // bwd: mask of the relu whose output gradient we produce
+  uint32_t* mask_out;            // fwd: mask bits of this conv's relu
+  HL16 out;                      // full-res output (fwd relu output / bwd gradient)
+  HL16 out_pool;                 // fwd pooled output
+  HL16 content_v, content_u;     // bwd content term operands (same grid as out)
+  float content_coef;            // 2*lambda (0 = none)
+  HL16 addend;                   // bwd addend at out's grid (hi == nullptr: none)
+  int store_full;                // fwd pool: also store full-res relu output
+  // channel sums of the relu output over rows [sum_r0, sum_r1) (fwd, tap layers)
+  float* colsum_partial;         // [tiles_y*tiles_x][C_out_p], nullable
+  int sum_r0, sum_r1;
+  unsigned int* amax;            // max |output| (unscaled) as float bits
+};
+
+struct GramArgs {
+  CUtensorMap tm_hi, tm_lo;      // tap tensor viewed as (8, P, kg): box (8, 64, 16)
+  int C_p;                       // channels (padded)
+  long long p_begin, p_end;      // pixel range (flattened row-major over the tap grid)
+  int px_per_split;
+  int n_ctile;                   // channel tiles of 128
+  float* partial;                // [split][pair][128][128]
+};
+
+struct FirstConvArgs {
+  const float* img;   // (h, w, 3) f32, unpadded global image
+  int h, w;           // unpadded global dims
+  int row_off;        // global padded row of local row 0
+  int Hl, Wp;         // local grid (rows) x padded width
+  int perm[3];
+  float mean[3], scale[3];
+  const float* wgt;   // [C_out][3][3][3] f32
+  const float* bias;  // [C_out]
+  int C_out, C_out_p;
+  HL16 out;
+  uint32_t* mask;
+  float* colsum_partial;  // [blocks][C_out_p] nullable
+  int sum_r0, sum_r1;     // local rows contributing to sums
+  unsigned int* amax;
+};
+
+struct FirstConvBwdArgs {
+  HL16 g;             // gradient at the first conv's output (masked), C_p channels
+  const float* wgt;   // [C_out][3][3][3]
+  int C_out;
+  int perm[3];
+  float scale[3];
+  float* gimg;        // (Hl, Wp, 3) f32 local padded grid
+};
+
+struct StyleCoefArgs {
+  const double* S;      // [C][C] global sum of outer products
+  const double* s;      // [C] global channel sums
+  double n;             // global pixel count n_p
+  const double* Gr;     // style reference gram [C][C]
+  const double* mur;    // [C]
+  const double* sdr;    // [C]
+  double wg, wm, ws;    // TapWeights
+  int C;
+  double* mu;           // [C]
+  double* sd;           // [C]
+  double* ratio;        // [C]
+  float* bvec;          // [C_p] (zero padded)
+  double* row_loss;     // [C] sum_j (G-Gr)^2 per row
+  double* row_mmax;     // [C] max_j |M_kj| per row
+  double* ms_loss;      // [2]: sum (mu-mur)^2, sum (sd-sdr)^2
+  int* degenerate;      // set to 1 when sd < eps and sdr > eps
+  // extra-K weight slab for the backward kernel: [ntile][xkc][pass][kg][n][8] fp16
+  __half* xw;
+  int N, n_xkc;
+  float xscale;         // 2^f_M
+};
+
+struct AxpyDotArgs {
+  const float* q_in;
+  float* q_out;
+  const float* v;       // axpy vector (nullable)
+  const double* coef;   // device scalar: coefficient of v
+  double cscale;        // host-known multiplier of the whole result (gamma or -1)
+  const float* w;       // dot vector (nullable)
+  long long n;
+  double* partial;
+};
+
+// ---------------------------------------------------------------- launchers
+cudaError_t launch_conv_tc(const ConvArgs& a, int N, int grid, cudaStream_t stream);
+int conv_tc_smem_bytes(int N);
+cudaError_t launch_gram_tc(const GramArgs& a, int n_splits, cudaStream_t stream);
+cudaError_t launch_gram_reduce(const float* partial, int n_splits, int n_ctile, int C, double inv_scale2,
+                               double* S, cudaStream_t stream);
+cudaError_t launch_first_conv_fwd(const FirstConvArgs& a, cudaStream_t st);
+int first_conv_fwd_blocks(int Hl, int Wp);
+cudaError_t launch_first_conv_bwd(const FirstConvBwdArgs& a, cudaStream_t st);
+cudaError_t launch_fold_grad(const float* gimg, int Hl, int Wp, int row_off, int h, int w, int r0, int r1,
+                             float* grad, cudaStream_t st);
+cudaError_t launch_pool2_hl(const HL16& in, const HL16& out, unsigned int* amax, cudaStream_t st);
+cudaError_t launch_colsum_reduce(const float* partial, int rows, int C, double* sums, cudaStream_t st);
+cudaError_t launch_style_vec(const StyleCoefArgs& a, cudaStream_t st);
+cudaError_t launch_style_mat(const StyleCoefArgs& a, cudaStream_t st);
+cudaError_t launch_content_sqdiff(const HL16& v, const HL16& u, int C, int r0, int r1, double* partial,
+                                  double* out, cudaStream_t st);
+cudaError_t launch_dots(const float* a0, const float* b0, const float* a1, const float* b1, const float* a2,
+                        const float* b2, long long n, double* partial, double* out, cudaStream_t st);
+cudaError_t launch_absmax(const float* a, long long n, float* partial, float* out, cudaStream_t st);
+cudaError_t launch_axpy_dot(const AxpyDotArgs& a, cudaStream_t st);
+cudaError_t launch_twoloop_scalar(const double* partial, double rho, int mode, double* alpha_i, double* coef,
+                                  cudaStream_t st);
+cudaError_t launch_sum_partials(const double* partial, int nk, double* out, cudaStream_t st);
+cudaError_t launch_axpy(const float* x, const float* d, float t, long long n, float* out, cudaStream_t st);
+cudaError_t launch_sy(const float* xt, const float* x, const float* gt, const float* g, long long n, float* s,
+                      float* y, double* partial, double* out, cudaStream_t st);
+cudaError_t launch_resize_down(const float* in, int h, int w, int c, int f, float* out, cudaStream_t st);
+cudaError_t launch_resize_bilinear(const float* in, int h, int w, int c, int oh, int ow, float* out,
+                                   cudaStream_t st);
+int red_blocks();
+
+}  // namespace spst

@@ -1,0 +1,1223 @@
+// runtime.cu — native runtime behind the C ABI (include/spst.h): network plan, weight
+// staging into tensor-core layouts, HBM workspace, TMA descriptors, and the forward /
+// finalize / backward schedules of Algorithm 1 (reference localized.py:162-311), plus the
+// exported vector and resampling kernels.
+//
+// Range management for the fp16 hi/lo operands: every stored tensor carries a power-of-two
+// scale chosen from the max |value| observed the previous time it was written (kernels
+// record it with atomicMax).  The first time a tensor is produced the stage is checked
+// immediately and re-run with the measured exponent if the stored range was off; later
+// evaluations run without host syncs and fall back to that careful mode only if a range
+// check at the end of the pass fails.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/spst.h"
+#include "common.cuh"
+#include "sm100.cuh"
+
+using namespace spst;
+
+namespace {
+
+constexpr int kPxPerSplit = 8192;    // Gram pixels summed per fp32 TMEM accumulator
+constexpr float kTargetLog2 = 11.f;  // stored |max| ~ 2^11 (fp16 max 65504 ~ 2^16)
+constexpr float kOverflow = 30000.f;
+constexpr float kUnderflow = 64.f;
+
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+bool get_encoder() {
+  if (g_encode) return true;
+  cudaDriverEntryPointQueryResult q;
+  void* fn = nullptr;
+  if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn) {
+    cudaGetLastError();
+    return false;
+  }
+  g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  return true;
+}
+
+bool map_act(CUtensorMap* m, const __half* base, int n_kg, int H, int W) {
+  cuuint64_t dims[4] = {8, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)n_kg};
+  cuuint64_t strides[3] = {16, (cuuint64_t)W * 16, (cuuint64_t)H * W * 16};
+  cuuint32_t box[4] = {8, 130, 4, 2};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  return g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, (void*)base, dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+bool map_gram(CUtensorMap* m, const __half* base, long long P_range, long long P_total, int n_kg) {
+  cuuint64_t dims[3] = {8, (cuuint64_t)P_range, (cuuint64_t)n_kg};
+  cuuint64_t strides[2] = {16, (cuuint64_t)P_total * 16};
+  cuuint32_t box[3] = {8, 64, 16};
+  cuuint32_t es[3] = {1, 1, 1};
+  return g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, (void*)base, dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+int round_up(int v, int m) { return (v + m - 1) / m * m; }
+int ntile_for(int C_p) { return (C_p % 128 == 0) ? 128 : 64; }
+float pow2f(int e) { return std::ldexp(1.0f, e); }
+int choose_exp(float amax) {
+  if (!(amax > 0.f) || !std::isfinite(amax)) return 0;
+  int e = (int)std::floor(kTargetLog2 - std::log2(amax));
+  return std::max(-40, std::min(90, e));
+}
+bool range_bad(float amax, float scale) {
+  return !std::isfinite(amax) || amax * scale > kOverflow || (amax > 0.f && amax * scale < kUnderflow);
+}
+float bits_to_float(unsigned int u) {
+  float f;
+  std::memcpy(&f, &u, 4);
+  return f;
+}
+void split_host(double v, __half& hi, __half& lo) {
+  hi = __float2half_rn((float)v);
+  lo = __float2half_rn((float)(v - (double)__half2float(hi)));
+}
+
+struct TapState {
+  int stage = -1;
+  double *S = nullptr, *s = nullptr, *Gr = nullptr, *mur = nullptr, *sdr = nullptr;
+  double *mu = nullptr, *sd = nullptr, *ratio = nullptr, *row_loss = nullptr, *row_mmax = nullptr,
+         *ms_loss = nullptr;
+  int* degenerate = nullptr;
+  float* bvec = nullptr;
+  __half* xw = nullptr;
+  double wg = 0, wm = 0, ws = 0, n = 0, mmax = 0;
+  bool has_ref = false;
+  float* gram_partial = nullptr;
+  int gram_splits = 0;
+  float* colsum_partial = nullptr;
+  int colsum_rows = 0;
+};
+
+struct Expo {
+  int e = 0;
+  bool known = false;
+};
+
+struct Stage {
+  int cin = 0, cout = 0, cin_p = 0, cout_p = 0;
+  bool pool_after = false;
+  int style = -1;
+  bool content = false;
+  int stride = 1;
+  std::vector<double> w, b;
+  int wexp = 0;
+  float* bias_d = nullptr;
+  float* w1_d = nullptr;
+  uint8_t* wf_d = nullptr;
+  uint8_t* wb_d = nullptr;
+  int H = 0, W = 0;
+  HL16 out, pooled;
+  bool has_out = false, store_out = false;
+  uint32_t* mask = nullptr;
+  Expo out_e, pool_e, g_e, add_e;
+  float g_written = 1.f;
+};
+
+}  // namespace
+
+struct spst_ctx {
+  int code = SPST_OK;
+  std::string msg;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::vector<Stage> stages;
+  std::vector<TapState> taps;
+  int content_stage = -1;
+  int perm[3] = {0, 1, 2};
+  float mean[3] = {0, 0, 0}, scale[3] = {1, 1, 1};
+  int deepest_stride = 1;
+  std::vector<void*> persistent;  // weights
+  std::vector<void*> allocs;      // bound workspace
+  long long alloc_bytes = 0;
+  bool bound = false;
+  int h = 0, w = 0, Hp = 0, Wp = 0, grid_r0 = 0, grid_r1 = 0, own_r0 = 0, own_r1 = 0;
+  unsigned int* amax_d = nullptr;  // [stages][4]: out, pooled, grad, addend
+  std::vector<unsigned int> amax_h;
+  HL16 gbuf[2];
+  size_t gbuf_elems = 0;
+  HL16 addend;
+  size_t addend_elems = 0;
+  float* gimg = nullptr;
+  HL16 content_u;
+  bool content_captured = false;
+  double* content_partial = nullptr;
+  __half* zero_xw = nullptr;
+  bool fwd_done = false, finalized = false;
+
+  int fail(int c, const std::string& m) {
+    code = c;
+    msg = m;
+    return c;
+  }
+  int cuda(cudaError_t e, const char* where) {
+    if (e == cudaSuccess) return SPST_OK;
+    cudaGetLastError();
+    return fail(e == cudaErrorMemoryAllocation ? SPST_ERR_OOM : SPST_ERR_CUDA,
+                std::string(where) + ": " + cudaGetErrorString(e));
+  }
+  template <typename T>
+  T* dalloc(size_t n, bool keep = false) {
+    void* p = nullptr;
+    if (n == 0) n = 1;
+    if (cudaMalloc(&p, n * sizeof(T)) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    (keep ? persistent : allocs).push_back(p);
+    if (!keep) alloc_bytes += (long long)(n * sizeof(T));
+    return reinterpret_cast<T*>(p);
+  }
+  void release_bound() {
+    if (stream) cudaStreamSynchronize(stream);
+    cudaDeviceSynchronize();
+    for (void* p : allocs) cudaFree(p);
+    allocs.clear();
+    alloc_bytes = 0;
+    bound = false;
+    fwd_done = finalized = content_captured = false;
+    for (auto& t : taps) {
+      t.S = t.s = t.mu = t.sd = t.ratio = t.row_loss = t.row_mmax = t.ms_loss = nullptr;
+      t.degenerate = nullptr;
+      t.bvec = nullptr;
+      t.xw = nullptr;
+      t.gram_partial = nullptr;
+      t.colsum_partial = nullptr;
+    }
+  }
+};
+
+#define CK(call)                               \
+  do {                                         \
+    int _r = ctx->cuda((call), #call);         \
+    if (_r) return _r;                         \
+  } while (0)
+#define TRY(call)          \
+  do {                     \
+    int _r = (call);       \
+    if (_r) return _r;     \
+  } while (0)
+
+namespace {
+
+// ------------------------------------------------------------------------------------------
+// weight staging: [nt][kc][pass][tap][kg][n][8]
+//   fwd: n -> output channel, k -> input channel
+//   bwd: adjoint conv: n -> input channel, k -> output channel, taps flipped (2-dy, 2-dx)
+// ------------------------------------------------------------------------------------------
+std::vector<__half> stage_slabs(const Stage& s, bool bwd, int N) {
+  const int K_p = bwd ? s.cout_p : s.cin_p;
+  const int N_p = bwd ? s.cin_p : s.cout_p;
+  const int nkc = K_p / 16, nnt = N_p / N;
+  std::vector<__half> out((size_t)nnt * nkc * 2 * 9 * 2 * N * 8);
+  const double sc = std::ldexp(1.0, s.wexp);
+  size_t idx = 0;
+  for (int nt = 0; nt < nnt; ++nt)
+    for (int kc = 0; kc < nkc; ++kc)
+      for (int pass = 0; pass < 2; ++pass)
+        for (int tap = 0; tap < 9; ++tap)
+          for (int kg = 0; kg < 2; ++kg)
+            for (int n = 0; n < N; ++n)
+              for (int e = 0; e < 8; ++e, ++idx) {
+                const int ng = nt * N + n, kk = kc * 16 + kg * 8 + e;
+                const int dy = tap / 3, dx = tap % 3;
+                const int co = bwd ? kk : ng, ci = bwd ? ng : kk;
+                const int ty = bwd ? 2 - dy : dy, tx = bwd ? 2 - dx : dx;
+                double v = 0.0;
+                if (co < s.cout && ci < s.cin) v = s.w[(((size_t)co * s.cin + ci) * 3 + ty) * 3 + tx] * sc;
+                __half hi, lo;
+                split_host(v, hi, lo);
+                out[idx] = pass == 0 ? hi : lo;
+              }
+  return out;
+}
+
+int parse_net(spst_ctx* ctx, int n_layers, const int* kinds, const int* cin, const int* cout,
+              const double* const* weights, const double* const* biases, int n_style, const int* style_layers,
+              int content_layer) {
+  int last = content_layer;
+  for (int i = 0; i < n_style; ++i) last = std::max(last, style_layers[i]);
+  if (last < 0 || last >= n_layers) return ctx->fail(SPST_ERR_CONFIG, "tap layer index out of range");
+  int i = 0, stride = 1, prev_c = 3;
+  while (i <= last) {
+    if (kinds[i] != SPST_LAYER_CONV)
+      return ctx->fail(SPST_ERR_UNSUPPORTED,
+                       "device path expects (conv, relu[, pool]) groups; layer " + std::to_string(i) + " breaks it");
+    if (i + 1 >= n_layers || kinds[i + 1] != SPST_LAYER_RELU)
+      return ctx->fail(SPST_ERR_UNSUPPORTED, "every conv must be followed by a relu on the device path");
+    Stage s;
+    s.cin = cin[i];
+    s.cout = cout[i];
+    if (s.cin != prev_c) return ctx->fail(SPST_ERR_SHAPE, "conv input channels do not chain");
+    s.cin_p = ctx->stages.empty() ? 3 : round_up(s.cin, 64);
+    s.cout_p = round_up(s.cout, 64);
+    s.stride = stride;
+    s.w.assign(weights[i], weights[i] + (size_t)s.cout * s.cin * 9);
+    s.b.assign(biases[i], biases[i] + s.cout);
+    double mx = 0;
+    for (double v : s.w) mx = std::max(mx, std::fabs(v));
+    s.wexp = mx > 0 ? (int)std::floor(std::log2(16384.0 / mx)) : 0;
+    const int relu_idx = i + 1;
+    for (int t = 0; t < n_style; ++t)
+      if (style_layers[t] == relu_idx) s.style = t;
+    s.content = content_layer == relu_idx;
+    i += 2;
+    if (i <= last && (kinds[i] == SPST_LAYER_AVGPOOL || kinds[i] == SPST_LAYER_MAXPOOL)) {
+      if (kinds[i] == SPST_LAYER_MAXPOOL)
+        return ctx->fail(SPST_ERR_UNSUPPORTED, "max pooling is not implemented on the device path");
+      s.pool_after = true;
+      stride *= 2;
+      ++i;
+    }
+    prev_c = s.cout;
+    ctx->stages.push_back(std::move(s));
+  }
+  ctx->taps.assign(n_style, TapState());
+  for (int t = 0; t < n_style; ++t) {
+    bool found = false;
+    for (size_t k = 0; k < ctx->stages.size(); ++k)
+      if (ctx->stages[k].style == t) {
+        ctx->taps[t].stage = (int)k;
+        found = true;
+      }
+    if (!found) return ctx->fail(SPST_ERR_CONFIG, "style tap " + std::to_string(t) + " is not a conv relu");
+  }
+  ctx->content_stage = -1;
+  for (size_t k = 0; k < ctx->stages.size(); ++k)
+    if (ctx->stages[k].content) ctx->content_stage = (int)k;
+  // deepest stride among taps (extractor.py:95-96)
+  ctx->deepest_stride = 1;
+  for (auto& t : ctx->taps) ctx->deepest_stride = std::max(ctx->deepest_stride, ctx->stages[t.stage].stride);
+  if (ctx->content_stage >= 0)
+    ctx->deepest_stride = std::max(ctx->deepest_stride, ctx->stages[ctx->content_stage].stride);
+  // the trailing pool of the last stage (if any) is never evaluated
+  ctx->stages.back().pool_after = false;
+  return SPST_OK;
+}
+
+int upload_weights(spst_ctx* ctx) {
+  for (size_t k = 0; k < ctx->stages.size(); ++k) {
+    Stage& s = ctx->stages[k];
+    std::vector<float> b32(s.cout_p, 0.f);
+    for (int c = 0; c < s.cout; ++c) b32[c] = (float)s.b[c];
+    s.bias_d = ctx->dalloc<float>(s.cout_p, true);
+    if (!s.bias_d) return ctx->fail(SPST_ERR_OOM, "bias upload");
+    CK(cudaMemcpy(s.bias_d, b32.data(), b32.size() * 4, cudaMemcpyHostToDevice));
+    if (k == 0) {
+      std::vector<float> w32(s.w.size());
+      for (size_t j = 0; j < w32.size(); ++j) w32[j] = (float)s.w[j];
+      s.w1_d = ctx->dalloc<float>(w32.size(), true);
+      if (!s.w1_d) return ctx->fail(SPST_ERR_OOM, "first-layer weights");
+      CK(cudaMemcpy(s.w1_d, w32.data(), w32.size() * 4, cudaMemcpyHostToDevice));
+    }
+    if (k > 0) {
+      auto wf = stage_slabs(s, false, ntile_for(s.cout_p));
+      s.wf_d = ctx->dalloc<uint8_t>(wf.size() * 2, true);
+      if (!s.wf_d) return ctx->fail(SPST_ERR_OOM, "forward weight slabs");
+      CK(cudaMemcpy(s.wf_d, wf.data(), wf.size() * 2, cudaMemcpyHostToDevice));
+      auto wb = stage_slabs(s, true, ntile_for(s.cin_p));
+      s.wb_d = ctx->dalloc<uint8_t>(wb.size() * 2, true);
+      if (!s.wb_d) return ctx->fail(SPST_ERR_OOM, "backward weight slabs");
+      CK(cudaMemcpy(s.wb_d, wb.data(), wb.size() * 2, cudaMemcpyHostToDevice));
+    }
+  }
+  return SPST_OK;
+}
+
+HL16 hl_shape(int C_p, int H, int W) {
+  HL16 t;
+  t.C_p = C_p;
+  t.H = H;
+  t.W = W;
+  t.scale = 1.f;
+  return t;
+}
+
+// ------------------------------------------------------------------------------------------
+// one tensor-core conv / GEMM launch
+// ------------------------------------------------------------------------------------------
+struct ConvLaunch {
+  const HL16* in = nullptr;      // conv K operand (nullptr: extra-K only)
+  const uint8_t* wslab = nullptr;
+  const HL16* v = nullptr;       // extra-K operand
+  const __half* xw = nullptr;
+  int n_xkc = 0;
+  int H = 0, W = 0;              // GEMM grid (conv output grid)
+  float acc_scale = 1.f;
+  ConvArgs a{};
+};
+
+int run_conv(spst_ctx* ctx, ConvLaunch& L) {
+  ConvArgs& a = L.a;
+  const HL16* in = L.in ? L.in : L.v;
+  const HL16* v = L.v ? L.v : in;
+  if (!map_act(&a.tm_a_hi, in->hi, in->C_p / 8, in->H, in->W) ||
+      !map_act(&a.tm_a_lo, in->lo(), in->C_p / 8, in->H, in->W) ||
+      !map_act(&a.tm_v_hi, v->hi, v->C_p / 8, v->H, v->W) || !map_act(&a.tm_v_lo, v->lo(), v->C_p / 8, v->H, v->W))
+    return ctx->fail(SPST_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+  a.wgt = L.in ? L.wslab : nullptr;
+  a.n_kc = L.in ? L.in->C_p / 16 : 0;
+  a.xwgt = reinterpret_cast<const uint8_t*>(L.xw);
+  a.n_xkc = L.n_xkc;
+  a.H = L.H;
+  a.W = L.W;
+  const int N = ntile_for(a.out.C_p);
+  a.n_ntiles = a.out.C_p / N;
+  a.tiles_x = (L.W + 127) / 128;
+  a.tiles_y = (L.H + 1) / 2;
+  a.acc_scale = L.acc_scale;
+  if (a.n_kc + a.n_xkc == 0) return ctx->fail(SPST_ERR_CONFIG, "empty GEMM");
+  const int tiles = a.tiles_x * a.tiles_y * a.n_ntiles;
+  CK(launch_conv_tc(a, N, std::min(tiles, kSMs), ctx->stream));
+  return SPST_OK;
+}
+
+float read_amax(spst_ctx* ctx, int slot) {
+  unsigned int v = 0;
+  cudaMemcpyAsync(&v, ctx->amax_d + slot, 4, cudaMemcpyDeviceToHost, ctx->stream);
+  cudaStreamSynchronize(ctx->stream);
+  return bits_to_float(v);
+}
+
+// ------------------------------------------------------------------------------------------
+// forward (extractor.py:171-197) + statistics (localized.py:162-184, stats.py:43-50)
+// ------------------------------------------------------------------------------------------
+int forward_stage(spst_ctx* ctx, int k, const float* x) {
+  Stage& s = ctx->stages[k];
+  const int own0 = (ctx->own_r0 - ctx->grid_r0) / s.stride, own1 = (ctx->own_r1 - ctx->grid_r0) / s.stride;
+  TapState* tap = s.style >= 0 ? &ctx->taps[s.style] : nullptr;
+  s.out.scale = pow2f(s.out_e.e);
+  s.pooled.scale = pow2f(s.pool_e.e);
+  CK(cudaMemsetAsync(ctx->amax_d + 4 * k, 0, 8, ctx->stream));
+  if (k == 0) {
+    FirstConvArgs a{};
+    a.img = x;
+    a.h = ctx->h;
+    a.w = ctx->w;
+    a.row_off = ctx->grid_r0;
+    a.Hl = s.H;
+    a.Wp = s.W;
+    for (int c = 0; c < 3; ++c) {
+      a.perm[c] = ctx->perm[c];
+      a.mean[c] = ctx->mean[c];
+      a.scale[c] = ctx->scale[c];
+    }
+    a.wgt = s.w1_d;
+    a.bias = s.bias_d;
+    a.C_out = s.cout;
+    a.C_out_p = s.cout_p;
+    a.out = s.out;
+    a.mask = s.mask;
+    a.colsum_partial = tap ? tap->colsum_partial : nullptr;
+    a.sum_r0 = own0;
+    a.sum_r1 = own1;
+    a.amax = ctx->amax_d + 4 * k;
+    CK(launch_first_conv_fwd(a, ctx->stream));
+    if (s.pool_after) CK(launch_pool2_hl(s.out, s.pooled, ctx->amax_d + 4 * k + 1, ctx->stream));
+    return SPST_OK;
+  }
+  const Stage& p = ctx->stages[k - 1];
+  const HL16& in = p.pool_after ? p.pooled : p.out;
+  ConvLaunch L;
+  L.in = &in;
+  L.wslab = s.wf_d;
+  L.H = s.H;
+  L.W = s.W;
+  L.acc_scale = 1.f / (in.scale * pow2f(s.wexp));
+  ConvArgs& a = L.a;
+  a.epi = s.pool_after ? EPI_FWD_POOL : EPI_FWD;
+  a.bias = s.bias_d;
+  a.mask_out = s.mask;
+  a.out = s.out;
+  a.out_pool = s.pooled;
+  a.store_full = s.store_out ? 1 : 0;
+  a.colsum_partial = tap ? tap->colsum_partial : nullptr;
+  a.sum_r0 = own0;
+  a.sum_r1 = own1;
+  a.amax = ctx->amax_d + 4 * k;
+  return run_conv(ctx, L);
+}
+
+int stage_stats(spst_ctx* ctx, int k) {
+  Stage& s = ctx->stages[k];
+  if (s.style < 0) return SPST_OK;
+  TapState& t = ctx->taps[s.style];
+  CK(launch_colsum_reduce(t.colsum_partial, t.colsum_rows, s.cout, t.s, ctx->stream));
+  const int own0 = (ctx->own_r0 - ctx->grid_r0) / s.stride, own1 = (ctx->own_r1 - ctx->grid_r0) / s.stride;
+  const long long P_total = (long long)s.H * s.W;
+  const long long p0 = (long long)own0 * s.W, p1 = (long long)own1 * s.W;
+  GramArgs g{};
+  if (!map_gram(&g.tm_hi, s.out.hi + p0 * 8, p1 - p0, P_total, s.cout_p / 8) ||
+      !map_gram(&g.tm_lo, s.out.lo() + p0 * 8, p1 - p0, P_total, s.cout_p / 8))
+    return ctx->fail(SPST_ERR_CUDA, "cuTensorMapEncodeTiled failed (gram)");
+  g.C_p = s.cout_p;
+  g.p_begin = 0;
+  g.p_end = p1 - p0;
+  g.px_per_split = kPxPerSplit;
+  g.n_ctile = (s.cout_p + 127) / 128;
+  g.partial = t.gram_partial;
+  CK(launch_gram_tc(g, t.gram_splits, ctx->stream));
+  const double inv2 = 1.0 / ((double)s.out.scale * (double)s.out.scale);
+  CK(launch_gram_reduce(t.gram_partial, t.gram_splits, g.n_ctile, s.cout, inv2, t.S, ctx->stream));
+  return SPST_OK;
+}
+
+bool stage_ranges_ok(spst_ctx* ctx, int k, float m0, float m1) {
+  const Stage& s = ctx->stages[k];
+  bool ok = true;
+  if (s.has_out && range_bad(m0, s.out.scale)) ok = false;
+  if (s.pool_after && range_bad(m1, s.pooled.scale)) ok = false;
+  return ok;
+}
+
+int do_forward(spst_ctx* ctx, const float* x, bool careful) {
+  const int n = (int)ctx->stages.size();
+  for (int k = 0; k < n; ++k) {
+    Stage& s = ctx->stages[k];
+    const bool check = careful || !s.out_e.known || (s.pool_after && !s.pool_e.known);
+    for (int attempt = 0; attempt < 6; ++attempt) {
+      TRY(forward_stage(ctx, k, x));
+      if (!check) break;
+      const float m0 = read_amax(ctx, 4 * k), m1 = read_amax(ctx, 4 * k + 1);
+      const bool ok = stage_ranges_ok(ctx, k, m0, m1);
+      if (s.has_out) s.out_e = {choose_exp(m0), true};
+      if (s.pool_after) s.pool_e = {choose_exp(m1), true};
+      if (ok) break;
+    }
+  }
+  for (int k = 0; k < n; ++k) TRY(stage_stats(ctx, k));
+  ctx->amax_h.resize(4 * n);
+  CK(cudaMemcpyAsync(ctx->amax_h.data(), ctx->amax_d, 16 * n, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  bool bad = false;
+  for (int k = 0; k < n; ++k) {
+    Stage& s = ctx->stages[k];
+    const float m0 = bits_to_float(ctx->amax_h[4 * k]), m1 = bits_to_float(ctx->amax_h[4 * k + 1]);
+    if (s.has_out && (!std::isfinite(m0) || m0 * s.out.scale > kOverflow)) bad = true;
+    if (s.pool_after && (!std::isfinite(m1) || m1 * s.pooled.scale > kOverflow)) bad = true;
+    // exponents for the next write; the data now stored keep the scale they were written with
+    if (s.has_out && m0 > 0 && std::isfinite(m0)) s.out_e = {choose_exp(m0), true};
+    if (s.pool_after && m1 > 0 && std::isfinite(m1)) s.pool_e = {choose_exp(m1), true};
+  }
+  return bad ? 1 : 0;
+}
+
+// ------------------------------------------------------------------------------------------
+// backward (extractor.py:200-214 with the tap gradients of stats.py:127-174)
+// ------------------------------------------------------------------------------------------
+StyleCoefArgs coef_args(spst_ctx* ctx, TapState& t) {
+  const Stage& s = ctx->stages[t.stage];
+  StyleCoefArgs a{};
+  a.S = t.S;
+  a.s = t.s;
+  a.n = t.n;
+  a.Gr = t.Gr;
+  a.mur = t.mur;
+  a.sdr = t.sdr;
+  a.wg = t.wg;
+  a.wm = t.wm;
+  a.ws = t.ws;
+  a.C = s.cout;
+  a.mu = t.mu;
+  a.sd = t.sd;
+  a.ratio = t.ratio;
+  a.bvec = t.bvec;
+  a.row_loss = t.row_loss;
+  a.row_mmax = t.row_mmax;
+  a.ms_loss = t.ms_loss;
+  a.degenerate = t.degenerate;
+  a.N = ntile_for(s.cout_p);
+  a.n_xkc = s.cout_p / 16;
+  return a;
+}
+
+// tap gradient slab for stage k with extra-K scale 2^xexp
+int write_xw(spst_ctx* ctx, int k, int xexp) {
+  Stage& s = ctx->stages[k];
+  if (s.style < 0) return SPST_OK;
+  TapState& t = ctx->taps[s.style];
+  StyleCoefArgs a = coef_args(ctx, t);
+  a.xw = t.xw;
+  a.xscale = pow2f(xexp);
+  CK(cudaMemsetAsync(t.xw, 0, (size_t)s.cout_p * s.cout_p * 2 * sizeof(__half), ctx->stream));
+  CK(launch_style_mat(a, ctx->stream));
+  return SPST_OK;
+}
+
+int gemm_only_xexp(spst_ctx* ctx, int k) {
+  const Stage& s = ctx->stages[k];
+  if (s.style < 0) return 0;
+  const double mm = ctx->taps[s.style].mmax;
+  return mm > 0 ? (int)std::floor(std::log2(16384.0 / mm)) : 0;
+}
+
+// tap gradient (V M + b + content) of stage k into `out` (GEMM with extra-K only)
+int tap_grad_gemm(spst_ctx* ctx, int k, HL16 out, bool with_mask, double two_lambda, int slot) {
+  Stage& s = ctx->stages[k];
+  const int xexp = gemm_only_xexp(ctx, k);
+  TRY(write_xw(ctx, k, xexp));
+  ConvLaunch L;
+  L.v = &s.out;
+  L.xw = s.style >= 0 ? ctx->taps[s.style].xw : ctx->zero_xw;
+  L.n_xkc = s.cout_p / 16;
+  L.H = s.H;
+  L.W = s.W;
+  L.acc_scale = 1.f / (s.out.scale * pow2f(xexp));
+  ConvArgs& a = L.a;
+  a.epi = EPI_BWD;
+  a.bias = s.style >= 0 ? ctx->taps[s.style].bvec : nullptr;
+  a.mask_in = with_mask ? s.mask : nullptr;
+  a.out = out;
+  if (s.content && two_lambda != 0.0) {
+    a.content_v = s.out;
+    a.content_u = ctx->content_u;
+    a.content_coef = (float)two_lambda;
+  }
+  a.amax = ctx->amax_d + slot;
+  return run_conv(ctx, L);
+}
+
+// produce g_k (gradient at stage k's conv output) into gbuf[dst] from g_{k+1} in gbuf[src]
+int backward_stage(spst_ctx* ctx, int k, int src, int dst, double two_lambda) {
+  Stage& s = ctx->stages[k];
+  Stage& nx = ctx->stages[k + 1];
+  HL16 gin = ctx->gbuf[src];  // shape set by the caller
+  HL16 gout = hl_shape(s.cout_p, s.H, s.W);
+  gout.hi = ctx->gbuf[dst].hi;
+  gout.scale = pow2f(s.g_e.e);
+  s.g_written = gout.scale;
+  const bool is_tap = s.style >= 0 || (s.content && two_lambda != 0.0);
+  ConvLaunch L;
+  L.in = &gin;
+  L.wslab = nx.wb_d;
+  L.H = nx.H;
+  L.W = nx.W;
+  const int acc_e = nx.g_e.e + nx.wexp;
+  L.acc_scale = 1.f / pow2f(acc_e);
+  ConvArgs& a = L.a;
+  a.out = gout;
+  a.mask_in = s.mask;
+  a.amax = ctx->amax_d + 4 * k + 2;
+  bool use_addend = false;
+  if (s.pool_after) {
+    a.epi = EPI_BWD_POOL;
+    use_addend = is_tap;
+  } else {
+    a.epi = EPI_BWD;
+    if (s.style >= 0) {
+      // fuse V*M as extra K-steps when the slab scale that matches the conv accumulator fits fp16
+      const int xexp = acc_e - (int)std::lround(std::log2(s.out.scale));
+      const double mm = ctx->taps[s.style].mmax * std::ldexp(1.0, xexp);
+      if (mm <= 16384.0 * 2 && (mm >= 16.0 || mm == 0.0)) {
+        TRY(write_xw(ctx, k, xexp));
+        L.v = &s.out;
+        L.xw = ctx->taps[s.style].xw;
+        L.n_xkc = s.cout_p / 16;
+        a.bias = ctx->taps[s.style].bvec;
+      } else {
+        use_addend = true;
+      }
+    }
+    if (s.content && two_lambda != 0.0 && !use_addend) {
+      a.content_v = s.out;
+      a.content_u = ctx->content_u;
+      a.content_coef = (float)two_lambda;
+    }
+  }
+  if (use_addend) {
+    HL16 ad = hl_shape(s.cout_p, s.H, s.W);
+    ad.hi = ctx->addend.hi;
+    for (int attempt = 0; attempt < 6; ++attempt) {
+      ad.scale = pow2f(s.add_e.e);
+      CK(cudaMemsetAsync(ctx->amax_d + 4 * k + 3, 0, 4, ctx->stream));
+      TRY(tap_grad_gemm(ctx, k, ad, false, two_lambda, 4 * k + 3));
+      const float m = read_amax(ctx, 4 * k + 3);
+      const bool ok = !range_bad(m, ad.scale);
+      s.add_e = {choose_exp(m), true};
+      if (ok) break;
+    }
+    a.addend = ad;
+    a.bias = nullptr;
+    L.v = nullptr;
+    L.xw = nullptr;
+    L.n_xkc = 0;
+  }
+  CK(cudaMemsetAsync(ctx->amax_d + 4 * k + 2, 0, 4, ctx->stream));
+  return run_conv(ctx, L);
+}
+
+int do_backward(spst_ctx* ctx, double two_lambda, float* grad, bool careful) {
+  const int n = (int)ctx->stages.size();
+  const int Lst = n - 1;
+  Stage& sl = ctx->stages[Lst];
+  int cur = 0;
+  // deepest tap: g_L = mask * tapgrad (extractor.py:204-209 for the first tap met in reverse)
+  for (int attempt = 0; attempt < 6; ++attempt) {
+    HL16 g = hl_shape(sl.cout_p, sl.H, sl.W);
+    g.hi = ctx->gbuf[cur].hi;
+    g.scale = pow2f(sl.g_e.e);
+    sl.g_written = g.scale;
+    ctx->gbuf[cur] = g;
+    CK(cudaMemsetAsync(ctx->amax_d + 4 * Lst + 2, 0, 4, ctx->stream));
+    TRY(tap_grad_gemm(ctx, Lst, g, true, two_lambda, 4 * Lst + 2));
+    if (!(careful || !sl.g_e.known)) break;
+    const float m = read_amax(ctx, 4 * Lst + 2);
+    const bool ok = !range_bad(m, g.scale);
+    if (m > 0) sl.g_e = {choose_exp(m), true};
+    if (ok || m == 0.f) break;
+  }
+  for (int k = Lst - 1; k >= 0; --k) {
+    Stage& s = ctx->stages[k];
+    const bool check = careful || !s.g_e.known;
+    for (int attempt = 0; attempt < 6; ++attempt) {
+      TRY(backward_stage(ctx, k, cur, cur ^ 1, two_lambda));
+      if (!check) break;
+      const float m = read_amax(ctx, 4 * k + 2);
+      const bool ok = !range_bad(m, s.g_written);
+      if (m > 0) s.g_e = {choose_exp(m), true};
+      if (ok || m == 0.f) break;
+    }
+    HL16 g = hl_shape(s.cout_p, s.H, s.W);
+    g.hi = ctx->gbuf[cur ^ 1].hi;
+    g.scale = s.g_written;
+    cur ^= 1;
+    ctx->gbuf[cur] = g;
+  }
+  // first conv adjoint + preprocess adjoint, then fold the replicate padding
+  Stage& s0 = ctx->stages[0];
+  FirstConvBwdArgs b{};
+  b.g = ctx->gbuf[cur];
+  b.wgt = s0.w1_d;
+  b.C_out = s0.cout;
+  for (int c = 0; c < 3; ++c) {
+    b.perm[c] = ctx->perm[c];
+    b.scale[c] = ctx->scale[c];
+  }
+  b.gimg = ctx->gimg;
+  CK(launch_first_conv_bwd(b, ctx->stream));
+  const int r0 = ctx->own_r0, r1 = std::min(ctx->own_r1, ctx->h);
+  CK(launch_fold_grad(ctx->gimg, s0.H, s0.W, ctx->grid_r0, ctx->h, ctx->w, r0, r1, grad, ctx->stream));
+  // end-of-pass range check (fast path)
+  ctx->amax_h.resize(4 * n);
+  CK(cudaMemcpyAsync(ctx->amax_h.data(), ctx->amax_d, 16 * n, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  bool bad = false;
+  for (int k = 0; k < n; ++k) {
+    Stage& s = ctx->stages[k];
+    const float m = bits_to_float(ctx->amax_h[4 * k + 2]);
+    if (!std::isfinite(m) || m * s.g_written > kOverflow) bad = true;
+    if (m > 0 && std::isfinite(m)) s.g_e = {choose_exp(m), true};
+  }
+  return bad ? 1 : 0;
+}
+
+int bind_alloc(spst_ctx* ctx) {
+  const int n = (int)ctx->stages.size();
+  const int Hl = ctx->grid_r1 - ctx->grid_r0;
+  size_t gmax = 0, admax = 0;
+  int max_cp = 64;
+  for (int k = 0; k < n; ++k) {
+    Stage& s = ctx->stages[k];
+    s.H = Hl / s.stride;
+    s.W = ctx->Wp / s.stride;
+    const bool tap = s.style >= 0 || s.content;
+    s.has_out = (k == 0) || !s.pool_after || tap;
+    s.store_out = s.pool_after && tap && k > 0;
+    s.out = hl_shape(s.cout_p, s.H, s.W);
+    if (s.has_out) {
+      s.out.hi = ctx->dalloc<__half>((size_t)s.cout_p * s.H * s.W * 2);
+      if (!s.out.hi) return ctx->fail(SPST_ERR_OOM, "activation buffer");
+    }
+    s.pooled = hl_shape(s.cout_p, s.H / 2, s.W / 2);
+    if (s.pool_after) {
+      s.pooled.hi = ctx->dalloc<__half>((size_t)s.cout_p * (s.H / 2) * (s.W / 2) * 2);
+      if (!s.pooled.hi) return ctx->fail(SPST_ERR_OOM, "pooled buffer");
+    }
+    s.mask = ctx->dalloc<uint32_t>((size_t)(s.cout_p / 32) * s.H * s.W);
+    if (!s.mask) return ctx->fail(SPST_ERR_OOM, "mask buffer");
+    gmax = std::max(gmax, (size_t)s.cout_p * s.H * s.W * 2);
+    if (tap) admax = std::max(admax, (size_t)s.cout_p * s.H * s.W * 2);
+    max_cp = std::max(max_cp, s.cout_p);
+    if (s.style >= 0) {
+      TapState& t = ctx->taps[s.style];
+      const int C = s.cout, Cp = s.cout_p;
+      t.S = ctx->dalloc<double>((size_t)C * C);
+      t.s = ctx->dalloc<double>(Cp);
+      t.mu = ctx->dalloc<double>(C);
+      t.sd = ctx->dalloc<double>(C);
+      t.ratio = ctx->dalloc<double>(C);
+      t.row_loss = ctx->dalloc<double>(C);
+      t.row_mmax = ctx->dalloc<double>(C);
+      t.ms_loss = ctx->dalloc<double>(2);
+      t.degenerate = ctx->dalloc<int>(1);
+      t.bvec = ctx->dalloc<float>(Cp);
+      t.xw = ctx->dalloc<__half>((size_t)Cp * Cp * 2);
+      const int own0 = (ctx->own_r0 - ctx->grid_r0) / s.stride, own1 = (ctx->own_r1 - ctx->grid_r0) / s.stride;
+      const long long own_px = (long long)(own1 - own0) * s.W;
+      t.gram_splits = (int)std::max<long long>(1, (own_px + kPxPerSplit - 1) / kPxPerSplit);
+      const int nct = (Cp + 127) / 128;
+      t.gram_partial = ctx->dalloc<float>((size_t)t.gram_splits * (nct * (nct + 1) / 2) * 128 * 128);
+      t.colsum_rows = k == 0 ? first_conv_fwd_blocks(s.H, s.W) : ((s.W + 127) / 128) * ((s.H + 1) / 2) * 4;
+      t.colsum_partial = ctx->dalloc<float>((size_t)t.colsum_rows * Cp);
+      if (!t.S || !t.s || !t.mu || !t.sd || !t.ratio || !t.row_loss || !t.row_mmax || !t.ms_loss || !t.degenerate ||
+          !t.bvec || !t.xw || !t.gram_partial || !t.colsum_partial)
+        return ctx->fail(SPST_ERR_OOM, "statistics buffers");
+      CK(cudaMemset(t.bvec, 0, Cp * 4));
+      CK(cudaMemset(t.s, 0, Cp * 8));
+      if (!t.Gr) {  // reference buffers persist across binds
+        t.Gr = ctx->dalloc<double>((size_t)C * C, true);
+        t.mur = ctx->dalloc<double>(C, true);
+        t.sdr = ctx->dalloc<double>(C, true);
+        if (!t.Gr || !t.mur || !t.sdr) return ctx->fail(SPST_ERR_OOM, "reference statistics");
+        CK(cudaMemset(t.Gr, 0, (size_t)C * C * 8));
+        CK(cudaMemset(t.mur, 0, C * 8));
+        CK(cudaMemset(t.sdr, 0, C * 8));
+      }
+    }
+  }
+  for (int b = 0; b < 2; ++b) {
+    ctx->gbuf[b] = hl_shape(64, 1, 1);
+    ctx->gbuf[b].hi = ctx->dalloc<__half>(gmax);
+    if (!ctx->gbuf[b].hi) return ctx->fail(SPST_ERR_OOM, "gradient buffers");
+  }
+  ctx->gbuf_elems = gmax;
+  ctx->addend = hl_shape(64, 1, 1);
+  ctx->addend.hi = ctx->dalloc<__half>(std::max<size_t>(admax, 16));
+  ctx->addend_elems = admax;
+  ctx->gimg = ctx->dalloc<float>((size_t)Hl * ctx->Wp * 3);
+  ctx->amax_d = ctx->dalloc<unsigned int>(4 * n);
+  ctx->content_partial = ctx->dalloc<double>(red_blocks() + 8);
+  ctx->zero_xw = ctx->dalloc<__half>((size_t)max_cp * max_cp * 2);
+  if (!ctx->addend.hi || !ctx->gimg || !ctx->amax_d || !ctx->content_partial || !ctx->zero_xw)
+    return ctx->fail(SPST_ERR_OOM, "workspace");
+  CK(cudaMemset(ctx->zero_xw, 0, (size_t)max_cp * max_cp * 2 * sizeof(__half)));
+  CK(cudaMemset(ctx->amax_d, 0, 16 * n));
+  if (ctx->content_stage >= 0) {
+    const Stage& s = ctx->stages[ctx->content_stage];
+    ctx->content_u = hl_shape(s.cout_p, s.H, s.W);
+    ctx->content_u.hi = ctx->dalloc<__half>((size_t)s.cout_p * s.H * s.W * 2);
+    if (!ctx->content_u.hi) return ctx->fail(SPST_ERR_OOM, "content target");
+  }
+  return SPST_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// debug helpers: CHW f32 <-> HL16
+// ------------------------------------------------------------------------------------------
+__global__ void pack_hl_kernel(const float* x, int C, HL16 t) {
+  const long long n = (long long)t.C_p * t.H * t.W;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(i / ((long long)t.H * t.W));
+    const long long p = i % ((long long)t.H * t.W);
+    const float v = c < C ? x[(size_t)c * t.H * t.W + p] : 0.f;
+    HalfPair hp = split_f16(v * t.scale);
+    const size_t off = (((size_t)(c >> 3)) * t.H * t.W + p) * 8 + (c & 7);
+    t.hi[off] = hp.hi;
+    t.lo()[off] = hp.lo;
+  }
+}
+
+__global__ void unpack_hl_kernel(HL16 t, int C, float* x) {
+  const long long n = (long long)C * t.H * t.W;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(i / ((long long)t.H * t.W));
+    const long long p = i % ((long long)t.H * t.W);
+    const size_t off = (((size_t)(c >> 3)) * t.H * t.W + p) * 8 + (c & 7);
+    x[i] = (__half2float(t.hi[off]) + __half2float(t.lo()[off])) / t.scale;
+  }
+}
+
+__global__ void unpack_mask_kernel(const uint32_t* m, int C, int H, int W, float* x) {
+  const long long n = (long long)C * H * W;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(i / ((long long)H * W));
+    const long long p = i % ((long long)H * W);
+    x[i] = (float)((m[(size_t)(c >> 5) * H * W + p] >> (c & 31)) & 1u);
+  }
+}
+
+}  // namespace
+
+// ==========================================================================================
+// C ABI
+// ==========================================================================================
+extern "C" {
+
+int spst_abi_version(void) { return SPST_ABI_VERSION; }
+
+const char* spst_status_string(int s) {
+  switch (s) {
+    case SPST_OK: return "ok";
+    case SPST_ERR_SHAPE: return "shape error";
+    case SPST_ERR_GEOMETRY: return "geometry error";
+    case SPST_ERR_CONFIG: return "config error";
+    case SPST_ERR_NONFINITE: return "non-finite value";
+    case SPST_ERR_CUDA: return "CUDA error";
+    case SPST_ERR_OOM: return "out of device memory";
+    case SPST_ERR_UNSUPPORTED: return "unsupported on the device path";
+    case SPST_ERR_EMPTY: return "empty statistics";
+    default: return "unknown status";
+  }
+}
+
+int spst_create(int device, int n_layers, const int* kinds, const int* cin, const int* cout,
+                const double* const* weights, const double* const* biases, int n_style, const int* style_layers,
+                int content_layer, int bgr, const double* mean3, const double* scale3, spst_ctx** out) {
+  *out = nullptr;
+  spst_ctx* ctx = new spst_ctx();
+  *out = ctx;
+  ctx->device = device;
+  if (cudaSetDevice(device) != cudaSuccess) {
+    cudaGetLastError();
+    return ctx->fail(SPST_ERR_CUDA, "cudaSetDevice failed (no CUDA device?)");
+  }
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10) return ctx->fail(SPST_ERR_CUDA, "libspst is built for sm_100a (B200); device is sm_" +
+                                                            std::to_string(prop.major) + std::to_string(prop.minor));
+  if (!get_encoder()) return ctx->fail(SPST_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  if (bgr) {
+    ctx->perm[0] = 2;
+    ctx->perm[2] = 0;
+  }
+  for (int c = 0; c < 3; ++c) {
+    ctx->mean[c] = (float)mean3[c];
+    ctx->scale[c] = (float)scale3[c];
+  }
+  TRY(parse_net(ctx, n_layers, kinds, cin, cout, weights, biases, n_style, style_layers, content_layer));
+  TRY(upload_weights(ctx));
+  return SPST_OK;
+}
+
+void spst_destroy(spst_ctx* ctx) {
+  if (!ctx) return;
+  ctx->release_bound();
+  for (void* p : ctx->persistent) cudaFree(p);
+  delete ctx;
+}
+
+const char* spst_last_error(const spst_ctx* ctx) { return ctx ? ctx->msg.c_str() : "null context"; }
+
+int spst_set_stream(spst_ctx* ctx, void* stream) {
+  ctx->stream = reinterpret_cast<cudaStream_t>(stream);
+  return SPST_OK;
+}
+
+int spst_bind(spst_ctx* ctx, int h, int w, int grid_r0, int grid_r1, int own_r0, int own_r1) {
+  const int ds = ctx->deepest_stride;
+  if (h < 1 || w < 1) return ctx->fail(SPST_ERR_SHAPE, "image dims must be >= 1");
+  const int Hp = round_up(h, ds), Wp = round_up(w, ds);
+  if (grid_r0 % ds || grid_r1 % ds || own_r0 % ds || (own_r1 % ds && own_r1 != Hp))
+    return ctx->fail(SPST_ERR_GEOMETRY, "row ranges must be multiples of the deepest stride");
+  if (!(0 <= grid_r0 && grid_r0 <= own_r0 && own_r0 < own_r1 && own_r1 <= grid_r1 && grid_r1 <= Hp))
+    return ctx->fail(SPST_ERR_GEOMETRY, "row ranges must nest: 0 <= grid_r0 <= own_r0 < own_r1 <= grid_r1 <= Hp");
+  if (ctx->bound && ctx->h == h && ctx->w == w && ctx->grid_r0 == grid_r0 && ctx->grid_r1 == grid_r1 &&
+      ctx->own_r0 == own_r0 && ctx->own_r1 == own_r1)
+    return SPST_OK;
+  ctx->release_bound();
+  ctx->h = h;
+  ctx->w = w;
+  ctx->Hp = Hp;
+  ctx->Wp = Wp;
+  ctx->grid_r0 = grid_r0;
+  ctx->grid_r1 = grid_r1;
+  ctx->own_r0 = own_r0;
+  ctx->own_r1 = own_r1;
+  int r = bind_alloc(ctx);
+  if (r) {
+    ctx->release_bound();
+    return r;
+  }
+  ctx->bound = true;
+  return SPST_OK;
+}
+
+int spst_padded_dims(const spst_ctx* ctx, int* Hp, int* Wp) {
+  *Hp = ctx->Hp;
+  *Wp = ctx->Wp;
+  return SPST_OK;
+}
+
+int spst_tap_info(const spst_ctx* ctx, int tap, int* channels, int* stride, long long* owned_pixels) {
+  if (tap < 0 || tap >= (int)ctx->taps.size()) return SPST_ERR_CONFIG;
+  const Stage& s = ctx->stages[ctx->taps[tap].stage];
+  *channels = s.cout;
+  *stride = s.stride;
+  *owned_pixels = ctx->bound ? (long long)((ctx->own_r1 - ctx->own_r0) / s.stride) * (ctx->Wp / s.stride) : 0;
+  return SPST_OK;
+}
+
+long long spst_workspace_bytes(const spst_ctx* ctx) { return ctx->alloc_bytes; }
+
+int spst_forward(spst_ctx* ctx, const float* x, int flags) {
+  (void)flags;
+  if (!ctx->bound) return ctx->fail(SPST_ERR_CONFIG, "spst_bind must precede spst_forward");
+  int r = do_forward(ctx, x, false);
+  if (r == 1) r = do_forward(ctx, x, true);
+  if (r == 1) return ctx->fail(SPST_ERR_NONFINITE, "activation range could not be represented (non-finite?)");
+  if (r) return r;
+  ctx->fwd_done = true;
+  ctx->finalized = false;
+  return SPST_OK;
+}
+
+int spst_stats_ptrs(spst_ctx* ctx, int tap, double** S, double** s) {
+  if (tap < 0 || tap >= (int)ctx->taps.size() || !ctx->bound) return ctx->fail(SPST_ERR_CONFIG, "bad tap / unbound");
+  *S = ctx->taps[tap].S;
+  *s = ctx->taps[tap].s;
+  return SPST_OK;
+}
+
+int spst_capture_content(spst_ctx* ctx) {
+  if (ctx->content_stage < 0) return ctx->fail(SPST_ERR_CONFIG, "network has no content tap");
+  if (!ctx->fwd_done) return ctx->fail(SPST_ERR_CONFIG, "no forward to capture");
+  const Stage& s = ctx->stages[ctx->content_stage];
+  CK(cudaMemcpyAsync(ctx->content_u.hi, s.out.hi, s.out.bytes(), cudaMemcpyDeviceToDevice, ctx->stream));
+  ctx->content_u.scale = s.out.scale;
+  ctx->content_captured = true;
+  return SPST_OK;
+}
+
+int spst_content_sqdiff(spst_ctx* ctx, double* out) {
+  if (!ctx->content_captured) return ctx->fail(SPST_ERR_CONFIG, "content target not captured");
+  const Stage& s = ctx->stages[ctx->content_stage];
+  const int r0 = (ctx->own_r0 - ctx->grid_r0) / s.stride, r1 = (ctx->own_r1 - ctx->grid_r0) / s.stride;
+  CK(launch_content_sqdiff(s.out, ctx->content_u, s.cout, r0, r1, ctx->content_partial, out, ctx->stream));
+  return SPST_OK;
+}
+
+int spst_set_style_ref(spst_ctx* ctx, int tap, const double* gram, const double* mean, const double* std_,
+                       double wg, double wm, double ws) {
+  if (tap < 0 || tap >= (int)ctx->taps.size()) return ctx->fail(SPST_ERR_CONFIG, "bad tap index");
+  TapState& t = ctx->taps[tap];
+  const int C = ctx->stages[t.stage].cout;
+  if (!t.Gr) {
+    t.Gr = ctx->dalloc<double>((size_t)C * C, true);
+    t.mur = ctx->dalloc<double>(C, true);
+    t.sdr = ctx->dalloc<double>(C, true);
+    if (!t.Gr || !t.mur || !t.sdr) return ctx->fail(SPST_ERR_OOM, "reference statistics");
+  }
+  CK(cudaMemcpy(t.Gr, gram, (size_t)C * C * 8, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(t.mur, mean, (size_t)C * 8, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(t.sdr, std_, (size_t)C * 8, cudaMemcpyHostToDevice));
+  t.wg = wg;
+  t.wm = wm;
+  t.ws = ws;
+  t.has_ref = true;
+  return SPST_OK;
+}
+
+int spst_finalize(spst_ctx* ctx, const long long* n, double* terms, int* degenerate) {
+  if (!ctx->fwd_done) return ctx->fail(SPST_ERR_CONFIG, "spst_forward must precede spst_finalize");
+  for (size_t i = 0; i < ctx->taps.size(); ++i) {
+    TapState& t = ctx->taps[i];
+    if (n[i] <= 0) return ctx->fail(SPST_ERR_EMPTY, "no feature pixels accumulated");
+    t.n = (double)n[i];
+    StyleCoefArgs a = coef_args(ctx, t);
+    CK(cudaMemsetAsync(t.degenerate, 0, 4, ctx->stream));
+    CK(launch_style_vec(a, ctx->stream));
+    CK(launch_style_mat(a, ctx->stream));
+  }
+  std::vector<double> buf;
+  for (size_t i = 0; i < ctx->taps.size(); ++i) {
+    TapState& t = ctx->taps[i];
+    const int C = ctx->stages[t.stage].cout;
+    buf.resize(2 * C + 2);
+    int deg = 0;
+    CK(cudaMemcpyAsync(buf.data(), t.row_loss, C * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(buf.data() + C, t.row_mmax, C * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(buf.data() + 2 * C, t.ms_loss, 16, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(&deg, t.degenerate, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    double g = 0, mm = 0;
+    for (int c = 0; c < C; ++c) {
+      g += buf[c];
+      mm = std::max(mm, buf[C + c]);
+    }
+    t.mmax = mm;
+    terms[3 * i + 0] = t.wg * g;
+    terms[3 * i + 1] = t.wm * buf[2 * C];
+    terms[3 * i + 2] = t.ws * buf[2 * C + 1];
+    if (degenerate) degenerate[i] = deg;
+  }
+  ctx->finalized = true;
+  return SPST_OK;
+}
+
+int spst_backward(spst_ctx* ctx, double two_lambda, float* grad) {
+  if (!ctx->finalized) return ctx->fail(SPST_ERR_CONFIG, "spst_finalize must precede spst_backward");
+  if (two_lambda != 0.0 && ctx->content_stage >= 0 && !ctx->content_captured)
+    return ctx->fail(SPST_ERR_CONFIG, "content weight is nonzero but no content target was captured");
+  int r = do_backward(ctx, two_lambda, grad, false);
+  if (r == 1) r = do_backward(ctx, two_lambda, grad, true);
+  if (r == 1) return ctx->fail(SPST_ERR_NONFINITE, "gradient range could not be represented (non-finite?)");
+  return r;
+}
+
+// ------------------------------------------------------------------------------------ vectors
+int spst_vec_partials(void) { return red_blocks(); }
+
+int spst_vec_dots(const float* a0, const float* b0, const float* a1, const float* b1, const float* a2,
+                  const float* b2, long long n, double* partial, double* out, void* stream) {
+  return launch_dots(a0, b0, a1, b1, a2, b2, n, partial, out, (cudaStream_t)stream) == cudaSuccess ? SPST_OK
+                                                                                                 : SPST_ERR_CUDA;
+}
+
+int spst_vec_absmax(const float* a, long long n, float* partial, float* out, void* stream) {
+  return launch_absmax(a, n, partial, out, (cudaStream_t)stream) == cudaSuccess ? SPST_OK : SPST_ERR_CUDA;
+}
+
+int spst_vec_axpy_dot(const float* q_in, float* q_out, const float* v, const double* coef, double cscale,
+                      const float* w, long long n, double* partial, void* stream) {
+  AxpyDotArgs a{q_in, q_out, v, coef, cscale, w, n, partial};
+  return launch_axpy_dot(a, (cudaStream_t)stream) == cudaSuccess ? SPST_OK : SPST_ERR_CUDA;
+}
+
+int spst_vec_twoloop_scalar(const double* partial, double rho, int mode, double* alpha, double* coef,
+                            void* stream) {
+  return launch_twoloop_scalar(partial, rho, mode, alpha, coef, (cudaStream_t)stream) == cudaSuccess
+             ? SPST_OK
+             : SPST_ERR_CUDA;
+}
+
+int spst_vec_sum_partials(const double* partial, int nk, double* out, void* stream) {
+  return launch_sum_partials(partial, nk, out, (cudaStream_t)stream) == cudaSuccess ? SPST_OK : SPST_ERR_CUDA;
+}
+
+int spst_vec_axpy(const float* x, const float* d, float t, long long n, float* out, void* stream) {
+  return launch_axpy(x, d, t, n, out, (cudaStream_t)stream) == cudaSuccess ? SPST_OK : SPST_ERR_CUDA;
+}
+
+int spst_vec_sy(const float* xt, const float* x, const float* gt, const float* g, long long n, float* s, float* y,
+                double* partial, double* out, void* stream) {
+  return launch_sy(xt, x, gt, g, n, s, y, partial, out, (cudaStream_t)stream) == cudaSuccess ? SPST_OK
+                                                                                            : SPST_ERR_CUDA;
+}
+
+int spst_resize_down(const float* in, int h, int w, int c, int f, float* out, void* stream) {
+  if (f < 1) return SPST_ERR_SHAPE;
+  return launch_resize_down(in, h, w, c, f, out, (cudaStream_t)stream) == cudaSuccess ? SPST_OK : SPST_ERR_CUDA;
+}
+
+int spst_resize_bilinear(const float* in, int h, int w, int c, int oh, int ow, float* out, void* stream) {
+  if (oh < 1 || ow < 1) return SPST_ERR_SHAPE;
+  return launch_resize_bilinear(in, h, w, c, oh, ow, out, (cudaStream_t)stream) == cudaSuccess ? SPST_OK
+                                                                                              : SPST_ERR_CUDA;
+}
+
+// ------------------------------------------------------------------------------------ debug
+int spst_debug_conv(int device, int mode, int cin, int cout, int H, int W, const float* x_host,
+                    const double* weight, const double* bias, float* y_host) {
+  if (cudaSetDevice(device) != cudaSuccess || !get_encoder()) return SPST_ERR_CUDA;
+  spst_ctx holder;
+  spst_ctx* ctx = &holder;
+  Stage s;
+  s.cin = cin;
+  s.cout = cout;
+  s.cin_p = round_up(cin, 64);
+  s.cout_p = round_up(cout, 64);
+  s.w.assign(weight, weight + (size_t)cout * cin * 9);
+  s.b.assign(bias, bias + cout);
+  double mx = 0;
+  for (double v : s.w) mx = std::max(mx, std::fabs(v));
+  s.wexp = mx > 0 ? (int)std::floor(std::log2(16384.0 / mx)) : 0;
+  const bool bwd = mode == 2;
+  const int Kc = bwd ? cout : cin, Kp = bwd ? s.cout_p : s.cin_p, Np = bwd ? s.cin_p : s.cout_p;
+  const int Nc = bwd ? cin : cout;
+  auto slab = stage_slabs(s, bwd, ntile_for(Np));
+  uint8_t* slab_d = ctx->dalloc<uint8_t>(slab.size() * 2);
+  float* xd = ctx->dalloc<float>((size_t)Kc * H * W);
+  HL16 in = hl_shape(Kp, H, W);
+  in.hi = ctx->dalloc<__half>((size_t)Kp * H * W * 2);
+  HL16 out = hl_shape(Np, H, W);
+  out.hi = ctx->dalloc<__half>((size_t)Np * H * W * 2);
+  out.scale = 1.f;
+  HL16 pooled = hl_shape(Np, H / 2, W / 2);
+  pooled.hi = ctx->dalloc<__half>((size_t)Np * std::max(1, H / 2) * std::max(1, W / 2) * 2);
+  float* bd = ctx->dalloc<float>(Np);
+  uint32_t* mask = ctx->dalloc<uint32_t>((size_t)(Np / 32) * H * W);
+  float* yd = ctx->dalloc<float>((size_t)Nc * H * W);
+  if (!slab_d || !xd || !in.hi || !out.hi || !pooled.hi || !bd || !mask || !yd) return SPST_ERR_OOM;
+  std::vector<float> b32(Np, 0.f);
+  if (!bwd)
+    for (int c = 0; c < cout; ++c) b32[c] = (float)bias[c];
+  CK(cudaMemcpy(bd, b32.data(), Np * 4, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(slab_d, slab.data(), slab.size() * 2, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(xd, x_host, (size_t)Kc * H * W * 4, cudaMemcpyHostToDevice));
+  pack_hl_kernel<<<512, 256>>>(xd, Kc, in);
+  ConvLaunch L;
+  L.in = &in;
+  L.wslab = slab_d;
+  L.H = H;
+  L.W = W;
+  L.acc_scale = 1.f / (in.scale * pow2f(s.wexp));
+  L.a.out = out;
+  L.a.out_pool = pooled;
+  L.a.bias = bwd ? nullptr : bd;
+  L.a.mask_out = mask;
+  L.a.epi = bwd ? EPI_BWD : (mode == 1 ? EPI_FWD_POOL : EPI_FWD);
+  L.a.store_full = 0;
+  TRY(run_conv(ctx, L));
+  CK(cudaDeviceSynchronize());
+  if (mode == 1) {
+    unpack_hl_kernel<<<512, 256>>>(pooled, Nc, yd);
+    CK(cudaMemcpy(y_host, yd, (size_t)Nc * (H / 2) * (W / 2) * 4, cudaMemcpyDeviceToHost));
+  } else if (mode == 3) {
+    unpack_mask_kernel<<<512, 256>>>(mask, Nc, H, W, yd);
+    CK(cudaMemcpy(y_host, yd, (size_t)Nc * H * W * 4, cudaMemcpyDeviceToHost));
+  } else {
+    unpack_hl_kernel<<<512, 256>>>(out, Nc, yd);
+    CK(cudaMemcpy(y_host, yd, (size_t)Nc * H * W * 4, cudaMemcpyDeviceToHost));
+  }
+  CK(cudaDeviceSynchronize());
+  ctx->release_bound();
+  return SPST_OK;
+}
+
+int spst_debug_gram(int device, int C, long long P, const float* f_host, double* S_host) {
+  if (cudaSetDevice(device) != cudaSuccess || !get_encoder()) return SPST_ERR_CUDA;
+  spst_ctx holder;
+  spst_ctx* ctx = &holder;
+  const int Cp = round_up(C, 64);
+  HL16 t = hl_shape(Cp, 1, (int)P);
+  t.hi = ctx->dalloc<__half>((size_t)Cp * P * 2);
+  float* fd = ctx->dalloc<float>((size_t)C * P);
+  const int splits = (int)std::max<long long>(1, (P + kPxPerSplit - 1) / kPxPerSplit);
+  const int nct = (Cp + 127) / 128;
+  float* part = ctx->dalloc<float>((size_t)splits * (nct * (nct + 1) / 2) * 128 * 128);
+  double* Sd = ctx->dalloc<double>((size_t)C * C);
+  if (!t.hi || !fd || !part || !Sd) return SPST_ERR_OOM;
+  CK(cudaMemcpy(fd, f_host, (size_t)C * P * 4, cudaMemcpyHostToDevice));
+  pack_hl_kernel<<<512, 256>>>(fd, C, t);
+  GramArgs g{};
+  if (!map_gram(&g.tm_hi, t.hi, P, P, Cp / 8) || !map_gram(&g.tm_lo, t.lo(), P, P, Cp / 8)) return SPST_ERR_CUDA;
+  g.C_p = Cp;
+  g.p_begin = 0;
+  g.p_end = P;
+  g.px_per_split = kPxPerSplit;
+  g.n_ctile = nct;
+  g.partial = part;
+  CK(launch_gram_tc(g, splits, nullptr));
+  CK(launch_gram_reduce(part, splits, nct, C, 1.0, Sd, nullptr));
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemcpy(S_host, Sd, (size_t)C * C * 8, cudaMemcpyDeviceToHost));
+  ctx->release_bound();
+  return SPST_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,664 @@
+// simt.cu — the HBM-bound and tiny kernels of the SPST path (no tensor-core work):
+//   * first conv layer (3 input channels, K = 27) fused with replicate padding
+//     (tensorops.py:201-209), preprocessing (extractor.py:151-155), bias, ReLU, mask bits
+//     and tap channel sums; and its adjoint fused with preprocess_backward (158-164)
+//   * fold of replicate-pad gradients (tensorops.py:212-229)
+//   * standalone 2x2 average pool (tensorops.py:99-101) for nets whose first ReLU is pooled
+//   * statistics finalisation and the closed-form style coefficients (stats.py:59-66,
+//     117-165), content squared distance (localized.py:257-267)
+//   * deterministic f64 reductions, L-BFGS vector passes (lbfgs.py:68-142)
+//   * area downsampling and half-pixel bilinear resampling (tensorops.py:136-185)
+#include "common.cuh"
+#include "sm100.cuh"
+
+namespace spst {
+
+// ------------------------------------------------------------------------------------------
+// first conv (C_in = 3)
+// ------------------------------------------------------------------------------------------
+
+constexpr int FC_BX = 32, FC_BY = 8;
+
+__device__ __forceinline__ float warp_transpose_sum32(float (&v)[32]) {
+  const uint32_t lane = threadIdx.x & 31;
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) {
+#pragma unroll
+    for (int i = 0; i < off; ++i) {
+      float send = (lane & off) ? v[i] : v[i + off];
+      float keep = (lane & off) ? v[i + off] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+    }
+  }
+  return v[0];
+}
+
+__global__ void __launch_bounds__(256) first_conv_fwd_kernel(const FirstConvArgs a) {
+  __shared__ float tile[3][FC_BY + 2][FC_BX + 2];
+  __shared__ float wsm[64 * 27];
+  __shared__ float csum[FC_BY][32];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int x0 = blockIdx.x * FC_BX, y0 = blockIdx.y * FC_BY;
+  for (int i = threadIdx.x; i < 3 * (FC_BY + 2) * (FC_BX + 2); i += blockDim.x) {
+    const int c = i / ((FC_BY + 2) * (FC_BX + 2));
+    const int r = (i / (FC_BX + 2)) % (FC_BY + 2);
+    const int cc = i % (FC_BX + 2);
+    const int yl = y0 - 1 + r, xl = x0 - 1 + cc;
+    float v = 0.f;
+    if (yl >= 0 && yl < a.Hl && xl >= 0 && xl < a.Wp) {
+      const int gy = min(yl + a.row_off, a.h - 1), gx = min(xl, a.w - 1);
+      v = (a.img[((size_t)gy * a.w + gx) * 3 + a.perm[c]] - a.mean[c]) / a.scale[c];
+    }
+    tile[c][r][cc] = v;
+  }
+  const int y = y0 + ty, x = x0 + tx;
+  const bool ok = y < a.Hl && x < a.Wp;
+  const bool in_sum = ok && y >= a.sum_r0 && y < a.sum_r1;
+  float amax = 0.f;
+  for (int cg = 0; cg < a.C_out_p; cg += 32) {
+    const int nc = min(32, a.C_out - cg);
+    __syncthreads();
+    for (int i = threadIdx.x; i < 32 * 27; i += blockDim.x) wsm[i] = (i / 27 < nc) ? a.wgt[(size_t)cg * 27 + i] : 0.f;
+    __syncthreads();
+    float v[32];
+    uint32_t bits = 0;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      float acc = (j < nc) ? a.bias[cg + j] : 0.f;
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
+          for (int dx = 0; dx < 3; ++dx) acc = fmaf(tile[c][ty + dy][tx + dx], wsm[j * 27 + c * 9 + dy * 3 + dx], acc);
+      bits |= (acc > 0.f ? 1u : 0u) << j;
+      v[j] = fmaxf(acc, 0.f);
+      amax = fmaxf(amax, ok ? v[j] : 0.f);
+    }
+    if (ok) {
+      a.mask[((size_t)(cg >> 5) * a.Hl + y) * a.Wp + x] = bits;
+      const int nkg = min(4, (a.C_out_p - cg) / 8);
+      for (int k = 0; k < nkg; ++k) {
+        __align__(16) __half hh[8];
+        __align__(16) __half ll[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          HalfPair p = split_f16(v[8 * k + e] * a.out.scale);
+          hh[e] = p.hi;
+          ll[e] = p.lo;
+        }
+        const size_t off = ((size_t)((cg >> 3) + k) * a.out.H + y) * a.out.W + x;
+        reinterpret_cast<uint4*>(a.out.hi)[off] = *reinterpret_cast<uint4*>(hh);
+        reinterpret_cast<uint4*>(a.out.lo())[off] = *reinterpret_cast<uint4*>(ll);
+      }
+    }
+    if (a.colsum_partial) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = in_sum ? v[j] : 0.f;
+      csum[ty][tx] = warp_transpose_sum32(v);
+      __syncthreads();
+      if (ty == 0) {
+        float s = 0.f;
+        for (int r = 0; r < FC_BY; ++r) s += csum[r][tx];
+        const size_t blk = (size_t)blockIdx.y * gridDim.x + blockIdx.x;
+        if (cg + tx < a.C_out_p) a.colsum_partial[blk * a.C_out_p + cg + tx] = s;
+      }
+    }
+  }
+  if (a.amax) {
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, off));
+    if (tx == 0 && amax > 0.f) atomicMax(a.amax, __float_as_uint(amax));
+  }
+}
+
+
+__global__ void __launch_bounds__(256) first_conv_bwd_kernel(const FirstConvBwdArgs a) {
+  constexpr int CH = 16;
+  __shared__ float tile[CH][FC_BY + 2][FC_BX + 2];
+  __shared__ float wsm[CH * 27];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int x0 = blockIdx.x * FC_BX, y0 = blockIdx.y * FC_BY;
+  const int H = a.g.H, W = a.g.W;
+  const float inv = 1.f / a.g.scale;
+  float acc[3] = {0.f, 0.f, 0.f};
+  for (int c0 = 0; c0 < a.g.C_p; c0 += CH) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < (CH / 8) * (FC_BY + 2) * (FC_BX + 2); i += blockDim.x) {
+      const int kg = i / ((FC_BY + 2) * (FC_BX + 2));
+      const int r = (i / (FC_BX + 2)) % (FC_BY + 2);
+      const int cc = i % (FC_BX + 2);
+      const int yy = y0 - 1 + r, xx = x0 - 1 + cc;
+      float v8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      if (yy >= 0 && yy < H && xx >= 0 && xx < W) {
+        const size_t off = ((size_t)((c0 >> 3) + kg) * H + yy) * W + xx;
+        uint4 hv = reinterpret_cast<const uint4*>(a.g.hi)[off];
+        uint4 lv = reinterpret_cast<const uint4*>(a.g.lo())[off];
+        const __half* hh = reinterpret_cast<const __half*>(&hv);
+        const __half* ll = reinterpret_cast<const __half*>(&lv);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) v8[e] = (__half2float(hh[e]) + __half2float(ll[e])) * inv;
+      }
+#pragma unroll
+      for (int e = 0; e < 8; ++e) tile[kg * 8 + e][r][cc] = v8[e];
+    }
+    for (int i = threadIdx.x; i < CH * 27; i += blockDim.x) {
+      const int co = c0 + i / 27;
+      wsm[i] = co < a.C_out ? a.wgt[(size_t)co * 27 + i % 27] : 0.f;
+    }
+    __syncthreads();
+    // g_in[y][x][ci] = sum_{co,dy,dx} g[co][y+1-dy][x+1-dx] * W[co][ci][dy][dx]
+#pragma unroll 4
+    for (int co = 0; co < CH; ++co)
+#pragma unroll
+      for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
+        for (int dx = 0; dx < 3; ++dx) {
+          const float gv = tile[co][ty + 2 - dy][tx + 2 - dx];
+#pragma unroll
+          for (int ci = 0; ci < 3; ++ci) acc[ci] = fmaf(gv, wsm[co * 27 + ci * 9 + dy * 3 + dx], acc[ci]);
+        }
+  }
+  const int y = y0 + ty, x = x0 + tx;
+  if (y < H && x < W) {
+    float* o = a.gimg + ((size_t)y * W + x) * 3;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) o[a.perm[c]] = acc[c] / a.scale[c];
+  }
+}
+
+// grad (rows [r0,r1) of the h x w unpadded image) from the local padded-grid gradient.
+__global__ void fold_grad_kernel(const float* gimg, int Hl, int Wp, int row_off, int h, int w, int r0, int r1,
+                                 float* grad) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long n = (long long)(r1 - r0) * w;
+  if (i >= n) return;
+  const int gy = r0 + (int)(i / w), gx = (int)(i % w);
+  const int ly = gy - row_off;
+  float acc[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) acc[c] = gimg[((size_t)ly * Wp + gx) * 3 + c];
+  const int Hp_loc_end = Hl;  // local rows beyond the image (ly >= h - row_off) fold onto h-1
+  if (gy == h - 1)
+    for (int yy = ly + 1; yy < Hp_loc_end; ++yy)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) acc[c] += gimg[((size_t)yy * Wp + gx) * 3 + c];
+  if (gx == w - 1)
+    for (int xx = w; xx < Wp; ++xx)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) acc[c] += gimg[((size_t)ly * Wp + xx) * 3 + c];
+  if (gy == h - 1 && gx == w - 1)
+    for (int yy = ly + 1; yy < Hp_loc_end; ++yy)
+      for (int xx = w; xx < Wp; ++xx)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) acc[c] += gimg[((size_t)yy * Wp + xx) * 3 + c];
+  float* o = grad + ((size_t)gy * w + gx) * 3;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) o[c] = acc[c];
+}
+
+// 2x2 average pool HL16 -> HL16 (used when the first conv's ReLU is followed by a pool).
+__global__ void pool2_hl_kernel(HL16 in, HL16 out, unsigned int* amax) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long n = (long long)(in.C_p / 8) * out.H * out.W;
+  float m = 0.f;
+  if (i < n) {
+    const int kg = (int)(i / ((long long)out.H * out.W));
+    const int rem = (int)(i % ((long long)out.H * out.W));
+    const int py = rem / out.W, px = rem % out.W;
+    float s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const float inv = 1.f / in.scale;
+    for (int dy = 0; dy < 2; ++dy)
+      for (int dx = 0; dx < 2; ++dx) {
+        const size_t off = ((size_t)kg * in.H + 2 * py + dy) * in.W + 2 * px + dx;
+        uint4 hv = reinterpret_cast<const uint4*>(in.hi)[off];
+        uint4 lv = reinterpret_cast<const uint4*>(in.lo())[off];
+        const __half* hh = reinterpret_cast<const __half*>(&hv);
+        const __half* ll = reinterpret_cast<const __half*>(&lv);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) s[e] += (__half2float(hh[e]) + __half2float(ll[e])) * inv;
+      }
+    __align__(16) __half oh[8];
+    __align__(16) __half ol[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const float v = s[e] * 0.25f;
+      m = fmaxf(m, fabsf(v));
+      HalfPair p = split_f16(v * out.scale);
+      oh[e] = p.hi;
+      ol[e] = p.lo;
+    }
+    const size_t off = ((size_t)kg * out.H + py) * out.W + px;
+    reinterpret_cast<uint4*>(out.hi)[off] = *reinterpret_cast<uint4*>(oh);
+    reinterpret_cast<uint4*>(out.lo())[off] = *reinterpret_cast<uint4*>(ol);
+  }
+  if (amax) {
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+    if ((threadIdx.x & 31) == 0 && m > 0.f) atomicMax(amax, __float_as_uint(m));
+  }
+}
+
+// sums[c] = sum_r partial[r][c] in f64, fixed row order
+__global__ void colsum_reduce_kernel(const float* partial, int rows, int C, double* sums) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  double acc = 0.0;
+  for (int r = 0; r < rows; ++r) acc += (double)partial[(size_t)r * C + c];
+  sums[c] = acc;
+}
+
+// ------------------------------------------------------------------------------------------
+// statistics finalisation + style coefficients (one tap)
+// ------------------------------------------------------------------------------------------
+
+constexpr double kStdEps = 1e-8;
+
+__global__ void style_vec_kernel(StyleCoefArgs a) {
+  __shared__ double red[2][256];
+  double lm = 0.0, ls = 0.0;
+  for (int c = threadIdx.x; c < a.C; c += blockDim.x) {
+    const double g = a.S[(size_t)c * a.C + c] / a.n;
+    const double m = a.s[c] / a.n;
+    const double sd = sqrt(fmax(g - m * m, 0.0));
+    a.mu[c] = m;
+    a.sd[c] = sd;
+    const bool dead = sd < kStdEps;
+    if (dead && a.sdr[c] > kStdEps) *a.degenerate = 1;
+    const double r = dead ? 0.0 : (sd - a.sdr[c]) / sd;
+    a.ratio[c] = r;
+    double b = 0.0;
+    if (a.wm != 0.0) b += (2.0 * a.wm / a.n) * (m - a.mur[c]);
+    if (a.ws != 0.0) b -= (2.0 * a.ws / a.n) * m * r;
+    a.bvec[c] = (float)b;
+    lm += (m - a.mur[c]) * (m - a.mur[c]);
+    ls += (sd - a.sdr[c]) * (sd - a.sdr[c]);
+  }
+  red[0][threadIdx.x] = lm;
+  red[1][threadIdx.x] = ls;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t0 = 0.0, t1 = 0.0;
+    for (int i = 0; i < blockDim.x; ++i) {
+      t0 += red[0][i];
+      t1 += red[1][i];
+    }
+    a.ms_loss[0] = t0;
+    a.ms_loss[1] = t1;
+  }
+}
+
+// one block per row k: M[k][n] = (4wg/n)(G-Gr)[k][n] + delta_kn (2ws/n) ratio[n]
+__global__ void style_mat_kernel(StyleCoefArgs a) {
+  __shared__ double red[256];
+  __shared__ double redm[256];
+  const int k = blockIdx.x;
+  double acc = 0.0, mm = 0.0;
+  const int kc = k >> 4, kg = (k >> 3) & 1, e = k & 7;
+  for (int n = threadIdx.x; n < a.C; n += blockDim.x) {
+    const double g = a.S[(size_t)k * a.C + n] / a.n;
+    const double d = g - a.Gr[(size_t)k * a.C + n];
+    acc += d * d;
+    double mv = (a.wg != 0.0) ? (4.0 * a.wg / a.n) * d : 0.0;
+    if (n == k && a.ws != 0.0) mv += (2.0 * a.ws / a.n) * a.ratio[n];
+    mm = fmax(mm, fabs(mv));
+    if (a.xw) {
+      const float v = (float)(mv * (double)a.xscale);
+      HalfPair p = split_f16(v);
+      const int nt = n / a.N, nl = n % a.N;
+      const size_t base = ((size_t)nt * a.n_xkc + kc) * 2;
+      a.xw[(((base + 0) * 2 + kg) * a.N + nl) * 8 + e] = p.hi;
+      a.xw[(((base + 1) * 2 + kg) * a.N + nl) * 8 + e] = p.lo;
+    }
+  }
+  red[threadIdx.x] = acc;
+  redm[threadIdx.x] = mm;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0, m = 0.0;
+    for (int i = 0; i < blockDim.x; ++i) {
+      t += red[i];
+      m = fmax(m, redm[i]);
+    }
+    a.row_loss[k] = t;
+    a.row_mmax[k] = m;
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// content squared distance over local rows [r0, r1): sum (V - Vu)^2 (f64 partials)
+// ------------------------------------------------------------------------------------------
+__global__ void content_sqdiff_kernel(HL16 v, HL16 u, int C, int r0, int r1, double* partial) {
+  __shared__ double red[256];
+  const long long per_plane = (long long)(r1 - r0) * v.W;
+  const long long n = (long long)(v.C_p / 8) * per_plane;
+  double acc = 0.0;
+  const float iv = 1.f / v.scale, iu = 1.f / u.scale;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const int kg = (int)(i / per_plane);
+    const long long rem = i % per_plane;
+    const size_t off = (size_t)kg * v.H * v.W + (size_t)r0 * v.W + rem;
+    uint4 vh = reinterpret_cast<const uint4*>(v.hi)[off];
+    uint4 vl = reinterpret_cast<const uint4*>(v.lo())[off];
+    uint4 uh = reinterpret_cast<const uint4*>(u.hi)[off];
+    uint4 ul = reinterpret_cast<const uint4*>(u.lo())[off];
+    const __half* a0 = reinterpret_cast<const __half*>(&vh);
+    const __half* a1 = reinterpret_cast<const __half*>(&vl);
+    const __half* b0 = reinterpret_cast<const __half*>(&uh);
+    const __half* b1 = reinterpret_cast<const __half*>(&ul);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      if (kg * 8 + e >= C) continue;
+      const float dv = (__half2float(a0[e]) + __half2float(a1[e])) * iv - (__half2float(b0[e]) + __half2float(b1[e])) * iu;
+      acc += (double)dv * (double)dv;
+    }
+  }
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial[blockIdx.x] = red[0];
+}
+
+// ------------------------------------------------------------------------------------------
+// deterministic reductions and L-BFGS vector passes
+// ------------------------------------------------------------------------------------------
+constexpr int kRedBlocks = 2 * kSMs;
+constexpr int kRedThreads = 512;
+
+template <typename T>
+__device__ __forceinline__ T block_sum(T v, T* sh) {
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  T t = 0;
+  if (threadIdx.x == 0)
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += sh[i];
+  return t;
+}
+
+// out[b] = partial dot products for up to 3 simultaneous pairs: <a0,b0>, <a1,b1>, <a2,b2>
+__global__ void __launch_bounds__(kRedThreads) dot3_partial_kernel(const float* a0, const float* b0, const float* a1,
+                                                                   const float* b1, const float* a2, const float* b2,
+                                                                   long long n, double* partial) {
+  __shared__ double sh[32];
+  double s0 = 0, s1 = 0, s2 = 0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    s0 += (double)a0[i] * (double)b0[i];
+    if (a1) s1 += (double)a1[i] * (double)b1[i];
+    if (a2) s2 += (double)a2[i] * (double)b2[i];
+  }
+  double t = block_sum(s0, sh);
+  __syncthreads();
+  if (threadIdx.x == 0) partial[blockIdx.x] = t;
+  if (a1) {
+    t = block_sum(s1, sh);
+    __syncthreads();
+    if (threadIdx.x == 0) partial[gridDim.x + blockIdx.x] = t;
+  }
+  if (a2) {
+    t = block_sum(s2, sh);
+    __syncthreads();
+    if (threadIdx.x == 0) partial[2 * gridDim.x + blockIdx.x] = t;
+  }
+}
+
+// out[k] = sum_b partial[k*nb + b], k < nk; optional out_scaled[k] = coef[k] * out[k]
+__global__ void finish_sums_kernel(const double* partial, int nb, int nk, double* out) {
+  const int k = threadIdx.x;
+  if (k >= nk) return;
+  double acc = 0.0;
+  for (int b = 0; b < nb; ++b) acc += partial[(size_t)k * nb + b];
+  out[k] = acc;
+}
+
+__global__ void __launch_bounds__(kRedThreads) absmax_partial_kernel(const float* a, long long n, float* partial) {
+  __shared__ float sh[32];
+  float m = 0.f;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    m = fmaxf(m, fabsf(a[i]));
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = 0.f;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t = fmaxf(t, sh[i]);
+    partial[blockIdx.x] = t;
+  }
+}
+
+// Two-loop step: q_out = cq * (q_in + coef * v), where coef = sign * scal[0] * (scal_k - scal_j)
+// style scalars live in device memory (see lbfgs_two_loop in runtime.cu), then partial <w, q_out>.
+
+__global__ void __launch_bounds__(kRedThreads) axpy_dot_kernel(AxpyDotArgs a) {
+  __shared__ double sh[32];
+  const float c = a.v ? (float)(*a.coef) : 0.f;
+  const float cs = (float)a.cscale;
+  double s = 0.0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += (long long)gridDim.x * blockDim.x) {
+    float q = a.q_in[i];
+    if (a.v) q = fmaf(c, a.v[i], q);
+    q *= cs;
+    a.q_out[i] = q;
+    if (a.w) s += (double)a.w[i] * (double)q;
+  }
+  if (a.w) {
+    const double t = block_sum(s, sh);
+    if (threadIdx.x == 0) a.partial[blockIdx.x] = t;
+  }
+}
+
+// scalar bookkeeping of the two-loop recursion on device
+// mode 0: alpha[i] = rho_i * dot ; coef = -alpha[i]
+// mode 1: beta = rho_i * dot ; coef = alpha[i] - beta
+__global__ void twoloop_scalar_kernel(const double* partial, int nb, double rho, int mode, double* alpha_i,
+                                      double* coef) {
+  double acc = 0.0;
+  for (int b = 0; b < nb; ++b) acc += partial[b];
+  if (mode == 0) {
+    *alpha_i = rho * acc;
+    *coef = -(*alpha_i);
+  } else {
+    *coef = *alpha_i - rho * acc;
+  }
+}
+
+// x_out = x + t*d (numpy weak-scalar semantics: t rounded to f32, product then sum)
+__global__ void axpy_kernel(const float* x, const float* d, float t, long long n, float* out) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    out[i] = __fadd_rn(x[i], __fmul_rn(t, d[i]));
+}
+
+// s = xt - x, y = gt - g and partials of <y,s>, <s,s>, <y,y>
+__global__ void __launch_bounds__(kRedThreads) sy_kernel(const float* xt, const float* x, const float* gt,
+                                                         const float* g, long long n, float* s, float* y,
+                                                         double* partial) {
+  __shared__ double sh[32];
+  double ys = 0, ss = 0, yy = 0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const float si = __fsub_rn(xt[i], x[i]);
+    const float yi = __fsub_rn(gt[i], g[i]);
+    s[i] = si;
+    y[i] = yi;
+    ys += (double)yi * si;
+    ss += (double)si * si;
+    yy += (double)yi * yi;
+  }
+  double t = block_sum(ys, sh);
+  __syncthreads();
+  if (threadIdx.x == 0) partial[blockIdx.x] = t;
+  t = block_sum(ss, sh);
+  __syncthreads();
+  if (threadIdx.x == 0) partial[gridDim.x + blockIdx.x] = t;
+  t = block_sum(yy, sh);
+  __syncthreads();
+  if (threadIdx.x == 0) partial[2 * gridDim.x + blockIdx.x] = t;
+}
+
+// ------------------------------------------------------------------------------------------
+// resampling (HWC f32)
+// ------------------------------------------------------------------------------------------
+__global__ void resize_down_kernel(const float* in, int h, int w, int c, int f, float* out) {
+  const int oh = (h + f - 1) / f, ow = (w + f - 1) / f;
+  const long long n = (long long)oh * ow * c;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const int ch = (int)(i % c);
+    const long long p = i / c;
+    const int oy = (int)(p / ow), ox = (int)(p % ow);
+    const int y0 = oy * f, y1 = min(y0 + f, h), x0 = ox * f, x1 = min(x0 + f, w);
+    // reference order: rows of each column summed first (reduceat axis 0), then columns
+    float tot = 0.f;
+    for (int xx = x0; xx < x1; ++xx) {
+      float col = 0.f;
+      for (int yy = y0; yy < y1; ++yy) col += in[((size_t)yy * w + xx) * c + ch];
+      tot += col;
+    }
+    const float area = (float)(y1 - y0) * (float)(x1 - x0);
+    out[i] = tot / area;
+  }
+}
+
+__device__ __forceinline__ void bilin_axis(int i, int n_in, int n_out, int& i0, int& i1, float& t) {
+  double s = ((double)i + 0.5) * ((double)n_in / (double)n_out) - 0.5;
+  s = fmin(fmax(s, 0.0), (double)n_in - 1.0);
+  i0 = (int)floor(s);
+  i1 = min(i0 + 1, n_in - 1);
+  t = (float)(s - (double)i0);
+}
+
+__global__ void resize_bilinear_kernel(const float* in, int h, int w, int c, int oh, int ow, float* out) {
+  const long long n = (long long)oh * ow * c;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const int ch = (int)(i % c);
+    const long long p = i / c;
+    const int oy = (int)(p / ow), ox = (int)(p % ow);
+    int y0, y1, x0, x1;
+    float ty, tx;
+    bilin_axis(oy, h, oh, y0, y1, ty);
+    bilin_axis(ox, w, ow, x0, x1, tx);
+    const float omy = 1.f - ty, omx = 1.f - tx;
+    const float r0 = __fadd_rn(__fmul_rn(in[((size_t)y0 * w + x0) * c + ch], omy), __fmul_rn(in[((size_t)y1 * w + x0) * c + ch], ty));
+    const float r1 = __fadd_rn(__fmul_rn(in[((size_t)y0 * w + x1) * c + ch], omy), __fmul_rn(in[((size_t)y1 * w + x1) * c + ch], ty));
+    out[i] = __fadd_rn(__fmul_rn(r0, omx), __fmul_rn(r1, tx));
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// launch helpers
+// ------------------------------------------------------------------------------------------
+cudaError_t launch_first_conv_fwd(const FirstConvArgs& a, cudaStream_t st) {
+  dim3 grid((a.Wp + FC_BX - 1) / FC_BX, (a.Hl + FC_BY - 1) / FC_BY);
+  first_conv_fwd_kernel<<<grid, 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
+int first_conv_fwd_blocks(int Hl, int Wp) { return ((Wp + FC_BX - 1) / FC_BX) * ((Hl + FC_BY - 1) / FC_BY); }
+
+cudaError_t launch_first_conv_bwd(const FirstConvBwdArgs& a, cudaStream_t st) {
+  dim3 grid((a.g.W + FC_BX - 1) / FC_BX, (a.g.H + FC_BY - 1) / FC_BY);
+  first_conv_bwd_kernel<<<grid, 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fold_grad(const float* gimg, int Hl, int Wp, int row_off, int h, int w, int r0, int r1,
+                             float* grad, cudaStream_t st) {
+  const long long n = (long long)(r1 - r0) * w;
+  if (n <= 0) return cudaSuccess;
+  fold_grad_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(gimg, Hl, Wp, row_off, h, w, r0, r1, grad);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pool2_hl(const HL16& in, const HL16& out, unsigned int* amax, cudaStream_t st) {
+  const long long n = (long long)(in.C_p / 8) * out.H * out.W;
+  pool2_hl_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(in, out, amax);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_colsum_reduce(const float* partial, int rows, int C, double* sums, cudaStream_t st) {
+  colsum_reduce_kernel<<<(C + 127) / 128, 128, 0, st>>>(partial, rows, C, sums);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_style_vec(const StyleCoefArgs& a, cudaStream_t st) {
+  style_vec_kernel<<<1, 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_style_mat(const StyleCoefArgs& a, cudaStream_t st) {
+  style_mat_kernel<<<a.C, 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sum_partials(const double* partial, int nk, double* out, cudaStream_t st) {
+  finish_sums_kernel<<<1, 32, 0, st>>>(partial, kRedBlocks, nk, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_content_sqdiff(const HL16& v, const HL16& u, int C, int r0, int r1, double* partial,
+                                  double* out, cudaStream_t st) {
+  content_sqdiff_kernel<<<kRedBlocks, 256, 0, st>>>(v, u, C, r0, r1, partial);
+  finish_sums_kernel<<<1, 32, 0, st>>>(partial, kRedBlocks, 1, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dots(const float* a0, const float* b0, const float* a1, const float* b1, const float* a2,
+                        const float* b2, long long n, double* partial, double* out, cudaStream_t st) {
+  dot3_partial_kernel<<<kRedBlocks, kRedThreads, 0, st>>>(a0, b0, a1, b1, a2, b2, n, partial);
+  const int nk = 1 + (a1 != nullptr) + (a2 != nullptr);
+  finish_sums_kernel<<<1, 32, 0, st>>>(partial, kRedBlocks, nk, out);
+  return cudaGetLastError();
+}
+
+__global__ void finish_max_kernel(const float* partial, int nb, float* out) {
+  float m = 0.f;
+  for (int b = 0; b < nb; ++b) m = fmaxf(m, partial[b]);
+  *out = m;
+}
+
+cudaError_t launch_absmax(const float* a, long long n, float* partial, float* out, cudaStream_t st) {
+  absmax_partial_kernel<<<kRedBlocks, kRedThreads, 0, st>>>(a, n, partial);
+  finish_max_kernel<<<1, 1, 0, st>>>(partial, kRedBlocks, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_axpy_dot(const AxpyDotArgs& a, cudaStream_t st) {
+  axpy_dot_kernel<<<kRedBlocks, kRedThreads, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_twoloop_scalar(const double* partial, double rho, int mode, double* alpha_i, double* coef,
+                                  cudaStream_t st) {
+  twoloop_scalar_kernel<<<1, 1, 0, st>>>(partial, kRedBlocks, rho, mode, alpha_i, coef);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_axpy(const float* x, const float* d, float t, long long n, float* out, cudaStream_t st) {
+  axpy_kernel<<<4 * kSMs, 512, 0, st>>>(x, d, t, n, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sy(const float* xt, const float* x, const float* gt, const float* g, long long n, float* s,
+                      float* y, double* partial, double* out, cudaStream_t st) {
+  sy_kernel<<<kRedBlocks, kRedThreads, 0, st>>>(xt, x, gt, g, n, s, y, partial);
+  finish_sums_kernel<<<1, 32, 0, st>>>(partial, kRedBlocks, 3, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_resize_down(const float* in, int h, int w, int c, int f, float* out, cudaStream_t st) {
+  resize_down_kernel<<<4 * kSMs, 256, 0, st>>>(in, h, w, c, f, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_resize_bilinear(const float* in, int h, int w, int c, int oh, int ow, float* out,
+                                   cudaStream_t st) {
+  resize_bilinear_kernel<<<4 * kSMs, 256, 0, st>>>(in, h, w, c, oh, ow, out);
+  return cudaGetLastError();
+}
+
+int red_blocks() { return kRedBlocks; }
+
+}  // namespace spst

@@ -1,0 +1,131 @@
+"""Style statistics records, loss weights and the host-side accumulator API.
+
+Mirrors the reference stats module's public data model (reference stats.py:22-124,
+181-200): ``LayerStats``, ``StatsAccumulator`` (f64 merge/finalize), ``TapWeights``,
+``LossWeights``, ``default_loss_weights``, ``style_loss_terms`` and the stats file format.
+On the device path the per-pixel work (Gram contraction, feature gradients) runs in
+libspst.so; what remains here is the O(C^2) host bookkeeping of finalised statistics.
+"""
+
+from __future__ import annotations
+
+import warnings
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import formats
+from .errors import EmptyError, ShapeError
+
+STD_EPS = 1e-8  # stats.py:19
+
+
+@dataclass(frozen=True)
+class LayerStats:
+    gram: np.ndarray   # (n_c, n_c)
+    mean: np.ndarray   # (n_c,)
+    std: np.ndarray    # (n_c,)
+    n_p: int
+
+    @property
+    def channels(self) -> int:
+        return self.mean.shape[0]
+
+
+def finalize_sums(S: np.ndarray, s: np.ndarray, n: int) -> LayerStats:
+    """G = S/n, mu = s/n, std = sqrt(max(diag G - mu^2, 0)) (stats.py:59-66)."""
+    if n == 0:
+        raise EmptyError("no feature pixels accumulated")
+    gram = S / n
+    mean = s / n
+    var = np.maximum(np.diagonal(gram) - mean ** 2, 0.0)
+    return LayerStats(gram=gram, mean=mean, std=np.sqrt(var), n_p=int(n))
+
+
+class StatsAccumulator:
+    """Streaming f64 sums (stats.py:34-66); device partials merge into it."""
+
+    def __init__(self, channels: int):
+        self.channels = channels
+        self.sum_outer = np.zeros((channels, channels))
+        self.sum = np.zeros(channels)
+        self.count = 0
+
+    def accumulate(self, features: np.ndarray) -> None:
+        if features.ndim != 3 or features.shape[0] != self.channels:
+            raise ShapeError(f"expected ({self.channels},h,w) features, got {features.shape}")
+        flat = features.reshape(self.channels, -1).astype(np.float64, copy=False)
+        self.sum_outer += flat @ flat.T
+        self.sum += flat.sum(axis=1)
+        self.count += flat.shape[1]
+
+    def add_sums(self, S: np.ndarray, s: np.ndarray, n: int) -> None:
+        self.sum_outer += S
+        self.sum += s
+        self.count += int(n)
+
+    def merge(self, other: "StatsAccumulator") -> None:
+        if other.channels != self.channels:
+            raise ShapeError(f"cannot merge {other.channels}-channel stats into {self.channels}")
+        self.add_sums(other.sum_outer, other.sum, other.count)
+
+    def finalize(self) -> LayerStats:
+        return finalize_sums(self.sum_outer, self.sum, self.count)
+
+
+@dataclass(frozen=True)
+class TapWeights:
+    gram: float
+    mean: float
+    std: float
+
+
+@dataclass(frozen=True)
+class LossWeights:
+    lambda_c: float
+    style: dict
+
+    def __post_init__(self):
+        vals = [self.lambda_c] + [v for w in self.style.values() for v in (w.gram, w.mean, w.std)]
+        if any(v < 0 for v in vals):
+            raise ShapeError("loss weights must be >= 0")
+        if not any(v > 0 for v in vals):
+            warnings.warn("all loss weights are zero; the objective is identically 0", stacklevel=2)
+
+
+def default_loss_weights(spec, lambda_c: float = 1.0, mean_std_factor: float = 1e3) -> LossWeights:
+    """w_gram = 1/n_c^2, w_mean = w_std = factor/n_c^2 (stats.py:98-110)."""
+    from .spec import tap_geometry
+    style = {}
+    for t in spec.style_taps:
+        c = tap_geometry(spec, t).channels
+        style[t] = TapWeights(1.0 / c ** 2, mean_std_factor / c ** 2, mean_std_factor / c ** 2)
+    return LossWeights(lambda_c=lambda_c, style=style)
+
+
+def style_loss_terms(sx: LayerStats, sr: LayerStats, w: TapWeights) -> tuple:
+    """(w_g |G-G_ref|^2, w_m |mu-mu_ref|^2, w_s |std-std_ref|^2) (stats.py:117-124)."""
+    if sx.channels != sr.channels:
+        raise ShapeError(f"stats have {sx.channels} vs {sr.channels} channels")
+    return (w.gram * float(np.sum((sx.gram - sr.gram) ** 2)),
+            w.mean * float(np.sum((sx.mean - sr.mean) ** 2)),
+            w.std * float(np.sum((sx.std - sr.std) ** 2)))
+
+
+def save_stats(path, stats: dict) -> None:
+    recs = {}
+    for tap, s in stats.items():
+        recs[f"{tap}.gram"] = s.gram
+        recs[f"{tap}.mean"] = s.mean
+        recs[f"{tap}.std"] = s.std
+        recs[f"{tap}.n_p"] = np.array([s.n_p], dtype=np.float64)
+    formats.write_records(path, recs)
+
+
+def load_stats(path) -> dict:
+    recs = formats.read_records(path)
+    out = {}
+    for tap in sorted({k.rsplit(".", 1)[0] for k in recs}):
+        out[tap] = LayerStats(recs[f"{tap}.gram"], recs[f"{tap}.mean"], recs[f"{tap}.std"],
+                              int(recs[f"{tap}.n_p"][0]))
+    return out

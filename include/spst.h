@@ -67,6 +67,7 @@ int spst_set_stream(spst_ctx* ctx, void* cuda_stream);
  * (statistics, content loss and gradient are restricted to owned rows; the rows outside
  * are the receptive-field halo). A single device binds grid = own = [0, Hp). */
 int spst_bind(spst_ctx* ctx, int h, int w, int grid_r0, int grid_r1, int own_r0, int own_r1);
+int spst_unbind(spst_ctx* ctx); /* release the bound workspace */
 int spst_padded_dims(const spst_ctx* ctx, int* Hp, int* Wp);
 int spst_tap_info(const spst_ctx* ctx, int tap, int* channels, int* stride, long long* owned_pixels);
 long long spst_workspace_bytes(const spst_ctx* ctx);
@@ -99,20 +100,23 @@ int spst_backward(spst_ctx* ctx, double two_lambda, float* grad_dev);
  * lbfgs.py:68-142. Reductions accumulate in f64 with a fixed order (deterministic). The
  * partial buffer must hold spst_vec_partials() doubles per reduced quantity. */
 int spst_vec_partials(void);
-int spst_vec_dots(const float* a0, const float* b0, const float* a1, const float* b1,
-                  const float* a2, const float* b2, long long n, double* partial_dev,
+/* f64 selects float64 vectors (1) or float32 vectors (0). */
+int spst_vec_dots(int f64, const void* a0, const void* b0, const void* a1, const void* b1,
+                  const void* a2, const void* b2, long long n, double* partial_dev,
                   double* out_dev, void* stream);
-int spst_vec_absmax(const float* a, long long n, float* partial_dev, float* out_dev, void* stream);
-/* q_out = cscale * (q_in + coef_dev[0] * v); partial <w, q_out> (w may be NULL). */
-int spst_vec_axpy_dot(const float* q_in, float* q_out, const float* v, const double* coef_dev,
-                      double cscale, const float* w, long long n, double* partial_dev, void* stream);
-/* mode 0: alpha_dev = rho*sum(partial), coef_dev = -alpha; mode 1: coef = alpha - rho*sum */
-int spst_vec_twoloop_scalar(const double* partial_dev, double rho, int mode, double* alpha_dev,
+int spst_vec_absmax(int f64, const void* a, long long n, double* partial_dev, double* out_dev,
+                    void* stream);
+/* q_out = cscale * (q_in + coef_dev[0] * v); partial <w, q_out> (v, w may be NULL). */
+int spst_vec_axpy_dot(int f64, const void* q_in, void* q_out, const void* v,
+                      const double* coef_dev, double cscale, const void* w, long long n,
+                      double* partial_dev, void* stream);
+/* finished dot -> mode 0: alpha = rho*dot, coef = -alpha; mode 1: coef = alpha - rho*dot */
+int spst_vec_twoloop_scalar(const double* dot_dev, double rho, int mode, double* alpha_dev,
                             double* coef_dev, void* stream);
 int spst_vec_sum_partials(const double* partial_dev, int n_quantities, double* out_dev, void* stream);
-int spst_vec_axpy(const float* x, const float* d, float t, long long n, float* out, void* stream);
-int spst_vec_sy(const float* xt, const float* x, const float* gt, const float* g, long long n,
-                float* s, float* y, double* partial_dev, double* out_dev /*[3]: ys, ss, yy*/,
+int spst_vec_axpy(int f64, const void* x, const void* d, double t, long long n, void* out, void* stream);
+int spst_vec_sy(int f64, const void* xt, const void* x, const void* gt, const void* g, long long n,
+                void* s, void* y, double* partial_dev, double* out_dev /*[3]: ys, ss, yy*/,
                 void* stream);
 
 /* ---------------------------------------------------------------- resampling ------------ */

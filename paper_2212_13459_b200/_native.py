@@ -40,6 +40,7 @@ SIGNATURES = {
     "spst_last_error": (ctypes.c_char_p, [c_void_p]),
     "spst_set_stream": (c_int, [c_void_p, c_void_p]),
     "spst_bind": (c_int, [c_void_p, c_int, c_int, c_int, c_int, c_int, c_int]),
+    "spst_unbind": (c_int, [c_void_p]),
     "spst_padded_dims": (c_int, [c_void_p, POINTER(c_int), POINTER(c_int)]),
     "spst_tap_info": (c_int, [c_void_p, c_int, POINTER(c_int), POINTER(c_int), POINTER(c_longlong)]),
     "spst_workspace_bytes": (c_longlong, [c_void_p]),
@@ -52,16 +53,16 @@ SIGNATURES = {
     "spst_finalize": (c_int, [c_void_p, POINTER(c_longlong), POINTER(c_double), POINTER(c_int)]),
     "spst_backward": (c_int, [c_void_p, c_double, c_void_p]),
     "spst_vec_partials": (c_int, []),
-    "spst_vec_dots": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_longlong, c_void_p,
-                              c_void_p, c_void_p]),
-    "spst_vec_absmax": (c_int, [c_void_p, c_longlong, c_void_p, c_void_p, c_void_p]),
-    "spst_vec_axpy_dot": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_double, c_void_p, c_longlong,
-                                  c_void_p, c_void_p]),
+    "spst_vec_dots": (c_int, [c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_longlong,
+                              c_void_p, c_void_p, c_void_p]),
+    "spst_vec_absmax": (c_int, [c_int, c_void_p, c_longlong, c_void_p, c_void_p, c_void_p]),
+    "spst_vec_axpy_dot": (c_int, [c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_double, c_void_p,
+                                  c_longlong, c_void_p, c_void_p]),
     "spst_vec_twoloop_scalar": (c_int, [c_void_p, c_double, c_int, c_void_p, c_void_p, c_void_p]),
     "spst_vec_sum_partials": (c_int, [c_void_p, c_int, c_void_p, c_void_p]),
-    "spst_vec_axpy": (c_int, [c_void_p, c_void_p, c_float, c_longlong, c_void_p, c_void_p]),
-    "spst_vec_sy": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_longlong, c_void_p, c_void_p, c_void_p,
-                            c_void_p, c_void_p]),
+    "spst_vec_axpy": (c_int, [c_int, c_void_p, c_void_p, c_double, c_longlong, c_void_p, c_void_p]),
+    "spst_vec_sy": (c_int, [c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_longlong, c_void_p, c_void_p,
+                            c_void_p, c_void_p, c_void_p]),
     "spst_resize_down": (c_int, [c_void_p, c_int, c_int, c_int, c_int, c_void_p, c_void_p]),
     "spst_resize_bilinear": (c_int, [c_void_p, c_int, c_int, c_int, c_int, c_int, c_void_p, c_void_p]),
     "spst_debug_conv": (c_int, [c_int, c_int, c_int, c_int, c_int, c_int, c_void_p, c_void_p, c_void_p,

@@ -117,12 +117,12 @@ struct StyleCoefArgs {
 };
 
 struct AxpyDotArgs {
-  const float* q_in;
-  float* q_out;
-  const float* v;       // axpy vector (nullable)
+  const void* q_in;     // f32 or f64 vectors (kernel template parameter)
+  void* q_out;
+  const void* v;        // axpy vector (nullable)
   const double* coef;   // device scalar: coefficient of v
   double cscale;        // host-known multiplier of the whole result (gamma or -1)
-  const float* w;       // dot vector (nullable)
+  const void* w;        // dot vector (nullable)
   long long n;
   double* partial;
 };
@@ -144,16 +144,16 @@ cudaError_t launch_style_vec(const StyleCoefArgs& a, cudaStream_t st);
 cudaError_t launch_style_mat(const StyleCoefArgs& a, cudaStream_t st);
 cudaError_t launch_content_sqdiff(const HL16& v, const HL16& u, int C, int r0, int r1, double* partial,
                                   double* out, cudaStream_t st);
-cudaError_t launch_dots(const float* a0, const float* b0, const float* a1, const float* b1, const float* a2,
-                        const float* b2, long long n, double* partial, double* out, cudaStream_t st);
-cudaError_t launch_absmax(const float* a, long long n, float* partial, float* out, cudaStream_t st);
-cudaError_t launch_axpy_dot(const AxpyDotArgs& a, cudaStream_t st);
-cudaError_t launch_twoloop_scalar(const double* partial, double rho, int mode, double* alpha_i, double* coef,
+cudaError_t launch_dots(int f64, const void* a0, const void* b0, const void* a1, const void* b1, const void* a2,
+                        const void* b2, long long n, double* partial, double* out, cudaStream_t st);
+cudaError_t launch_absmax(int f64, const void* a, long long n, double* partial, double* out, cudaStream_t st);
+cudaError_t launch_axpy_dot(int f64, const AxpyDotArgs& a, cudaStream_t st);
+cudaError_t launch_twoloop_scalar(const double* dot, double rho, int mode, double* alpha_i, double* coef,
                                   cudaStream_t st);
 cudaError_t launch_sum_partials(const double* partial, int nk, double* out, cudaStream_t st);
-cudaError_t launch_axpy(const float* x, const float* d, float t, long long n, float* out, cudaStream_t st);
-cudaError_t launch_sy(const float* xt, const float* x, const float* gt, const float* g, long long n, float* s,
-                      float* y, double* partial, double* out, cudaStream_t st);
+cudaError_t launch_axpy(int f64, const void* x, const void* d, double t, long long n, void* out, cudaStream_t st);
+cudaError_t launch_sy(int f64, const void* xt, const void* x, const void* gt, const void* g, long long n, void* s,
+                      void* y, double* partial, double* out, cudaStream_t st);
 cudaError_t launch_resize_down(const float* in, int h, int w, int c, int f, float* out, cudaStream_t st);
 cudaError_t launch_resize_bilinear(const float* in, int h, int w, int c, int oh, int ow, float* out,
                                    cudaStream_t st);

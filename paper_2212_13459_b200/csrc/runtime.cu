@@ -947,6 +947,11 @@ int spst_bind(spst_ctx* ctx, int h, int w, int grid_r0, int grid_r1, int own_r0,
   return SPST_OK;
 }
 
+int spst_unbind(spst_ctx* ctx) {
+  ctx->release_bound();
+  return SPST_OK;
+}
+
 int spst_padded_dims(const spst_ctx* ctx, int* Hp, int* Wp) {
   *Hp = ctx->Hp;
   *Wp = ctx->Wp;
@@ -1072,41 +1077,40 @@ int spst_backward(spst_ctx* ctx, double two_lambda, float* grad) {
 // ------------------------------------------------------------------------------------ vectors
 int spst_vec_partials(void) { return red_blocks(); }
 
-int spst_vec_dots(const float* a0, const float* b0, const float* a1, const float* b1, const float* a2,
-                  const float* b2, long long n, double* partial, double* out, void* stream) {
-  return launch_dots(a0, b0, a1, b1, a2, b2, n, partial, out, (cudaStream_t)stream) == cudaSuccess ? SPST_OK
-                                                                                                 : SPST_ERR_CUDA;
-}
-
-int spst_vec_absmax(const float* a, long long n, float* partial, float* out, void* stream) {
-  return launch_absmax(a, n, partial, out, (cudaStream_t)stream) == cudaSuccess ? SPST_OK : SPST_ERR_CUDA;
-}
-
-int spst_vec_axpy_dot(const float* q_in, float* q_out, const float* v, const double* coef, double cscale,
-                      const float* w, long long n, double* partial, void* stream) {
-  AxpyDotArgs a{q_in, q_out, v, coef, cscale, w, n, partial};
-  return launch_axpy_dot(a, (cudaStream_t)stream) == cudaSuccess ? SPST_OK : SPST_ERR_CUDA;
-}
-
-int spst_vec_twoloop_scalar(const double* partial, double rho, int mode, double* alpha, double* coef,
-                            void* stream) {
-  return launch_twoloop_scalar(partial, rho, mode, alpha, coef, (cudaStream_t)stream) == cudaSuccess
+int spst_vec_dots(int f64, const void* a0, const void* b0, const void* a1, const void* b1, const void* a2,
+                  const void* b2, long long n, double* partial, double* out, void* stream) {
+  return launch_dots(f64, a0, b0, a1, b1, a2, b2, n, partial, out, (cudaStream_t)stream) == cudaSuccess
              ? SPST_OK
              : SPST_ERR_CUDA;
+}
+
+int spst_vec_absmax(int f64, const void* a, long long n, double* partial, double* out, void* stream) {
+  return launch_absmax(f64, a, n, partial, out, (cudaStream_t)stream) == cudaSuccess ? SPST_OK : SPST_ERR_CUDA;
+}
+
+int spst_vec_axpy_dot(int f64, const void* q_in, void* q_out, const void* v, const double* coef, double cscale,
+                      const void* w, long long n, double* partial, void* stream) {
+  AxpyDotArgs a{q_in, q_out, v, coef, cscale, w, n, partial};
+  return launch_axpy_dot(f64, a, (cudaStream_t)stream) == cudaSuccess ? SPST_OK : SPST_ERR_CUDA;
+}
+
+int spst_vec_twoloop_scalar(const double* dot, double rho, int mode, double* alpha, double* coef, void* stream) {
+  return launch_twoloop_scalar(dot, rho, mode, alpha, coef, (cudaStream_t)stream) == cudaSuccess ? SPST_OK
+                                                                                                : SPST_ERR_CUDA;
 }
 
 int spst_vec_sum_partials(const double* partial, int nk, double* out, void* stream) {
   return launch_sum_partials(partial, nk, out, (cudaStream_t)stream) == cudaSuccess ? SPST_OK : SPST_ERR_CUDA;
 }
 
-int spst_vec_axpy(const float* x, const float* d, float t, long long n, float* out, void* stream) {
-  return launch_axpy(x, d, t, n, out, (cudaStream_t)stream) == cudaSuccess ? SPST_OK : SPST_ERR_CUDA;
+int spst_vec_axpy(int f64, const void* x, const void* d, double t, long long n, void* out, void* stream) {
+  return launch_axpy(f64, x, d, t, n, out, (cudaStream_t)stream) == cudaSuccess ? SPST_OK : SPST_ERR_CUDA;
 }
 
-int spst_vec_sy(const float* xt, const float* x, const float* gt, const float* g, long long n, float* s, float* y,
+int spst_vec_sy(int f64, const void* xt, const void* x, const void* gt, const void* g, long long n, void* s, void* y,
                 double* partial, double* out, void* stream) {
-  return launch_sy(xt, x, gt, g, n, s, y, partial, out, (cudaStream_t)stream) == cudaSuccess ? SPST_OK
-                                                                                            : SPST_ERR_CUDA;
+  return launch_sy(f64, xt, x, gt, g, n, s, y, partial, out, (cudaStream_t)stream) == cudaSuccess ? SPST_OK
+                                                                                                : SPST_ERR_CUDA;
 }
 
 int spst_resize_down(const float* in, int h, int w, int c, int f, float* out, void* stream) {

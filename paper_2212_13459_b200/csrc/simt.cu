@@ -381,9 +381,10 @@ __device__ __forceinline__ T block_sum(T v, T* sh) {
   return t;
 }
 
-// out[b] = partial dot products for up to 3 simultaneous pairs: <a0,b0>, <a1,b1>, <a2,b2>
-__global__ void __launch_bounds__(kRedThreads) dot3_partial_kernel(const float* a0, const float* b0, const float* a1,
-                                                                   const float* b1, const float* a2, const float* b2,
+// partial dot products for up to 3 simultaneous pairs: <a0,b0>, <a1,b1>, <a2,b2>
+template <typename T>
+__global__ void __launch_bounds__(kRedThreads) dot3_partial_kernel(const T* a0, const T* b0, const T* a1,
+                                                                   const T* b1, const T* a2, const T* b2,
                                                                    long long n, double* partial) {
   __shared__ double sh[32];
   double s0 = 0, s1 = 0, s2 = 0;
@@ -407,7 +408,7 @@ __global__ void __launch_bounds__(kRedThreads) dot3_partial_kernel(const float* 
   }
 }
 
-// out[k] = sum_b partial[k*nb + b], k < nk; optional out_scaled[k] = coef[k] * out[k]
+// out[k] = sum_b partial[k*nb + b], k < nk (fixed order)
 __global__ void finish_sums_kernel(const double* partial, int nb, int nk, double* out) {
   const int k = threadIdx.x;
   if (k >= nk) return;
@@ -416,73 +417,82 @@ __global__ void finish_sums_kernel(const double* partial, int nb, int nk, double
   out[k] = acc;
 }
 
-__global__ void __launch_bounds__(kRedThreads) absmax_partial_kernel(const float* a, long long n, float* partial) {
-  __shared__ float sh[32];
-  float m = 0.f;
+template <typename T>
+__global__ void __launch_bounds__(kRedThreads) absmax_partial_kernel(const T* a, long long n, double* partial) {
+  __shared__ double sh[32];
+  double m = 0.0;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
-    m = fmaxf(m, fabsf(a[i]));
+    m = fmax(m, fabs((double)a[i]));
 #pragma unroll
-  for (int off = 16; off >= 1; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+  for (int off = 16; off >= 1; off >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));
   if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = m;
   __syncthreads();
   if (threadIdx.x == 0) {
-    float t = 0.f;
-    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t = fmaxf(t, sh[i]);
+    double t = 0.0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t = fmax(t, sh[i]);
     partial[blockIdx.x] = t;
   }
 }
 
-// Two-loop step: q_out = cq * (q_in + coef * v), where coef = sign * scal[0] * (scal_k - scal_j)
-// style scalars live in device memory (see lbfgs_two_loop in runtime.cu), then partial <w, q_out>.
+__global__ void finish_max_kernel(const double* partial, int nb, double* out) {
+  double m = 0.0;
+  for (int b = 0; b < nb; ++b) m = fmax(m, partial[b]);
+  *out = m;
+}
 
+// Two-loop step: q_out = cscale * (q_in + coef[0] * v); partial <w, q_out>.
+template <typename T>
 __global__ void __launch_bounds__(kRedThreads) axpy_dot_kernel(AxpyDotArgs a) {
   __shared__ double sh[32];
-  const float c = a.v ? (float)(*a.coef) : 0.f;
-  const float cs = (float)a.cscale;
+  const T* qi = reinterpret_cast<const T*>(a.q_in);
+  T* qo = reinterpret_cast<T*>(a.q_out);
+  const T* v = reinterpret_cast<const T*>(a.v);
+  const T* w = reinterpret_cast<const T*>(a.w);
+  const T c = v ? (T)(*a.coef) : (T)0;
+  const T cs = (T)a.cscale;
   double s = 0.0;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += (long long)gridDim.x * blockDim.x) {
-    float q = a.q_in[i];
-    if (a.v) q = fmaf(c, a.v[i], q);
-    q *= cs;
-    a.q_out[i] = q;
-    if (a.w) s += (double)a.w[i] * (double)q;
+    T q = qi[i];
+    if (v) q = q + c * v[i];
+    q = q * cs;
+    qo[i] = q;
+    if (w) s += (double)w[i] * (double)q;
   }
-  if (a.w) {
+  if (w) {
     const double t = block_sum(s, sh);
     if (threadIdx.x == 0) a.partial[blockIdx.x] = t;
   }
 }
 
-// scalar bookkeeping of the two-loop recursion on device
-// mode 0: alpha[i] = rho_i * dot ; coef = -alpha[i]
-// mode 1: beta = rho_i * dot ; coef = alpha[i] - beta
-__global__ void twoloop_scalar_kernel(const double* partial, int nb, double rho, int mode, double* alpha_i,
-                                      double* coef) {
-  double acc = 0.0;
-  for (int b = 0; b < nb; ++b) acc += partial[b];
+// two-loop scalar bookkeeping from a finished (and possibly all-reduced) dot product
+// mode 0: alpha_i = rho * dot, coef = -alpha_i;  mode 1: coef = alpha_i - rho * dot
+__global__ void twoloop_scalar_kernel(const double* dot, double rho, int mode, double* alpha_i, double* coef) {
   if (mode == 0) {
-    *alpha_i = rho * acc;
+    *alpha_i = rho * (*dot);
     *coef = -(*alpha_i);
   } else {
-    *coef = *alpha_i - rho * acc;
+    *coef = *alpha_i - rho * (*dot);
   }
 }
 
-// x_out = x + t*d (numpy weak-scalar semantics: t rounded to f32, product then sum)
-__global__ void axpy_kernel(const float* x, const float* d, float t, long long n, float* out) {
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
-    out[i] = __fadd_rn(x[i], __fmul_rn(t, d[i]));
+// x_out = x + t*d (numpy weak-scalar semantics: t has x's dtype, product rounded then sum)
+template <typename T>
+__global__ void axpy_kernel(const T* x, const T* d, T t, long long n, T* out) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const T p = t * d[i];
+    out[i] = x[i] + p;
+  }
 }
 
 // s = xt - x, y = gt - g and partials of <y,s>, <s,s>, <y,y>
-__global__ void __launch_bounds__(kRedThreads) sy_kernel(const float* xt, const float* x, const float* gt,
-                                                         const float* g, long long n, float* s, float* y,
-                                                         double* partial) {
+template <typename T>
+__global__ void __launch_bounds__(kRedThreads) sy_kernel(const T* xt, const T* x, const T* gt, const T* g,
+                                                         long long n, T* s, T* y, double* partial) {
   __shared__ double sh[32];
   double ys = 0, ss = 0, yy = 0;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    const float si = __fsub_rn(xt[i], x[i]);
-    const float yi = __fsub_rn(gt[i], g[i]);
+    const T si = xt[i] - x[i];
+    const T yi = gt[i] - g[i];
     s[i] = si;
     y[i] = yi;
     ys += (double)yi * si;
@@ -605,45 +615,62 @@ cudaError_t launch_content_sqdiff(const HL16& v, const HL16& u, int C, int r0, i
   return cudaGetLastError();
 }
 
-cudaError_t launch_dots(const float* a0, const float* b0, const float* a1, const float* b1, const float* a2,
-                        const float* b2, long long n, double* partial, double* out, cudaStream_t st) {
-  dot3_partial_kernel<<<kRedBlocks, kRedThreads, 0, st>>>(a0, b0, a1, b1, a2, b2, n, partial);
+cudaError_t launch_dots(int f64, const void* a0, const void* b0, const void* a1, const void* b1, const void* a2,
+                        const void* b2, long long n, double* partial, double* out, cudaStream_t st) {
+  if (f64)
+    dot3_partial_kernel<double><<<kRedBlocks, kRedThreads, 0, st>>>(
+        (const double*)a0, (const double*)b0, (const double*)a1, (const double*)b1, (const double*)a2,
+        (const double*)b2, n, partial);
+  else
+    dot3_partial_kernel<float><<<kRedBlocks, kRedThreads, 0, st>>>((const float*)a0, (const float*)b0,
+                                                                   (const float*)a1, (const float*)b1,
+                                                                   (const float*)a2, (const float*)b2, n, partial);
   const int nk = 1 + (a1 != nullptr) + (a2 != nullptr);
   finish_sums_kernel<<<1, 32, 0, st>>>(partial, kRedBlocks, nk, out);
   return cudaGetLastError();
 }
 
-__global__ void finish_max_kernel(const float* partial, int nb, float* out) {
-  float m = 0.f;
-  for (int b = 0; b < nb; ++b) m = fmaxf(m, partial[b]);
-  *out = m;
-}
-
-cudaError_t launch_absmax(const float* a, long long n, float* partial, float* out, cudaStream_t st) {
-  absmax_partial_kernel<<<kRedBlocks, kRedThreads, 0, st>>>(a, n, partial);
+cudaError_t launch_absmax(int f64, const void* a, long long n, double* partial, double* out, cudaStream_t st) {
+  if (f64)
+    absmax_partial_kernel<double><<<kRedBlocks, kRedThreads, 0, st>>>((const double*)a, n, partial);
+  else
+    absmax_partial_kernel<float><<<kRedBlocks, kRedThreads, 0, st>>>((const float*)a, n, partial);
   finish_max_kernel<<<1, 1, 0, st>>>(partial, kRedBlocks, out);
   return cudaGetLastError();
 }
 
-cudaError_t launch_axpy_dot(const AxpyDotArgs& a, cudaStream_t st) {
-  axpy_dot_kernel<<<kRedBlocks, kRedThreads, 0, st>>>(a);
+cudaError_t launch_axpy_dot(int f64, const AxpyDotArgs& a, cudaStream_t st) {
+  if (f64)
+    axpy_dot_kernel<double><<<kRedBlocks, kRedThreads, 0, st>>>(a);
+  else
+    axpy_dot_kernel<float><<<kRedBlocks, kRedThreads, 0, st>>>(a);
   return cudaGetLastError();
 }
 
-cudaError_t launch_twoloop_scalar(const double* partial, double rho, int mode, double* alpha_i, double* coef,
+cudaError_t launch_twoloop_scalar(const double* dot, double rho, int mode, double* alpha_i, double* coef,
                                   cudaStream_t st) {
-  twoloop_scalar_kernel<<<1, 1, 0, st>>>(partial, kRedBlocks, rho, mode, alpha_i, coef);
+  twoloop_scalar_kernel<<<1, 1, 0, st>>>(dot, rho, mode, alpha_i, coef);
   return cudaGetLastError();
 }
 
-cudaError_t launch_axpy(const float* x, const float* d, float t, long long n, float* out, cudaStream_t st) {
-  axpy_kernel<<<4 * kSMs, 512, 0, st>>>(x, d, t, n, out);
+
+
+cudaError_t launch_axpy(int f64, const void* x, const void* d, double t, long long n, void* out, cudaStream_t st) {
+  if (f64)
+    axpy_kernel<double><<<4 * kSMs, 512, 0, st>>>((const double*)x, (const double*)d, t, n, (double*)out);
+  else
+    axpy_kernel<float><<<4 * kSMs, 512, 0, st>>>((const float*)x, (const float*)d, (float)t, n, (float*)out);
   return cudaGetLastError();
 }
 
-cudaError_t launch_sy(const float* xt, const float* x, const float* gt, const float* g, long long n, float* s,
-                      float* y, double* partial, double* out, cudaStream_t st) {
-  sy_kernel<<<kRedBlocks, kRedThreads, 0, st>>>(xt, x, gt, g, n, s, y, partial);
+cudaError_t launch_sy(int f64, const void* xt, const void* x, const void* gt, const void* g, long long n, void* s,
+                      void* y, double* partial, double* out, cudaStream_t st) {
+  if (f64)
+    sy_kernel<double><<<kRedBlocks, kRedThreads, 0, st>>>((const double*)xt, (const double*)x, (const double*)gt,
+                                                          (const double*)g, n, (double*)s, (double*)y, partial);
+  else
+    sy_kernel<float><<<kRedBlocks, kRedThreads, 0, st>>>((const float*)xt, (const float*)x, (const float*)gt,
+                                                         (const float*)g, n, (float*)s, (float*)y, partial);
   finish_sums_kernel<<<1, 32, 0, st>>>(partial, kRedBlocks, 3, out);
   return cudaGetLastError();
 }

@@ -1,0 +1,212 @@
+"""Device engine: one libspst context per (extractor spec, device).
+
+``Engine`` owns the native context (weights staged in tensor-core layouts, HBM workspace)
+and exposes the steps of Algorithm 1 (reference localized.py:162-311) as device calls:
+``forward`` (activations, masks, per-tap Gram / channel sums), ``finalize`` (global
+statistics, loss terms, closed-form feature gradients), ``backward`` (pixel gradient).
+PyTorch is used only for device memory and the stream; every FLOP runs in libspst.so.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+import weakref
+
+import numpy as np
+import torch
+
+from . import _native as nat
+from .errors import ShapeError
+from .spec import check_device_supported, tap_geometry
+
+_KIND = {"conv": 0, "relu": 1}
+
+
+class _DevView:
+    """Expose a raw device pointer to torch via __cuda_array_interface__."""
+
+    def __init__(self, ptr, shape, typestr):
+        self.__cuda_array_interface__ = {"data": (int(ptr), False), "shape": tuple(shape),
+                                         "typestr": typestr, "version": 3}
+
+
+def device_view(ptr, shape, dtype="<f8"):
+    return torch.as_tensor(_DevView(ptr, shape, dtype), device="cuda")
+
+
+def require_cuda():
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2212_13459_b200 requires a CUDA (sm_100a) device; there is no CPU path")
+
+
+class Engine:
+    """Native SPST context for one extractor spec on one device."""
+
+    def __init__(self, spec, device: int = 0):
+        require_cuda()
+        check_device_supported(spec)
+        if not spec.has_weights():
+            raise ShapeError("extractor has no weights bound")
+        self.spec = spec
+        self.device = device
+        L = nat.lib()
+        layers = spec.layers[:spec.deepest_tap_index() + 1]
+        n = len(layers)
+        kinds = (ctypes.c_int * n)()
+        cin = (ctypes.c_int * n)()
+        cout = (ctypes.c_int * n)()
+        wp = (ctypes.POINTER(ctypes.c_double) * n)()
+        bp = (ctypes.POINTER(ctypes.c_double) * n)()
+        self._keep = []
+        for i, l in enumerate(layers):
+            if l.kind == "pool":
+                kinds[i] = 2 if l.pool == "avg" else 3
+            else:
+                kinds[i] = _KIND[l.kind]
+            if l.kind == "conv":
+                cin[i], cout[i] = l.in_ch, l.out_ch
+                w = np.ascontiguousarray(l.weight, dtype=np.float64)
+                b = np.ascontiguousarray(l.bias, dtype=np.float64)
+                self._keep += [w, b]
+                wp[i] = w.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+                bp[i] = b.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+        idx = spec.layer_index()
+        self.style_taps = tuple(spec.style_taps)
+        st = (ctypes.c_int * max(1, len(self.style_taps)))(*[idx[t] for t in self.style_taps])
+        pre = spec.preprocess
+        mean = (ctypes.c_double * 3)(*pre.mean)
+        scale = (ctypes.c_double * 3)(*pre.scale)
+        handle = ctypes.c_void_p()
+        with torch.cuda.device(device):
+            status = L.spst_create(device, n, kinds, cin, cout, wp, bp, len(self.style_taps), st,
+                                   idx[spec.content_tap], 1 if pre.channel_order == "bgr" else 0, mean, scale,
+                                   ctypes.byref(handle))
+        self._h = handle.value
+        if status != nat.OK:
+            msg = L.spst_last_error(self._h).decode() if self._h else ""
+            if self._h:
+                L.spst_destroy(self._h)
+                self._h = None
+            nat.check(status, None, f"spst_create: {msg}")
+        self._finalizer = weakref.finalize(self, L.spst_destroy, self._h)
+        self.geom = {t: tap_geometry(spec, t) for t in spec.taps}
+        self.bound = None
+        self.bind_epoch = 0
+        self.lock = threading.RLock()
+        self._terms = np.zeros(3 * max(1, len(self.style_taps)))
+        self._deg = (ctypes.c_int * max(1, len(self.style_taps)))()
+        self._content_out = None
+        self.last_forward_key = None
+
+    # ------------------------------------------------------------------ plumbing
+    def _check(self, status, what):
+        nat.check(status, self._h, what)
+
+    def stream(self):
+        s = torch.cuda.current_stream(self.device)
+        nat.lib().spst_set_stream(self._h, ctypes.c_void_p(s.cuda_stream))
+        return s
+
+    # ------------------------------------------------------------------ geometry
+    def bind(self, h, w, grid=None, own=None):
+        """Bind image dims; grid/own are padded-row ranges (default: the whole image)."""
+        s = self.spec.deepest_stride()
+        Hp = h + (-h) % s
+        grid = grid or (0, Hp)
+        own = own or grid
+        key = (h, w, grid, own)
+        if self.bound == key:
+            return
+        with torch.cuda.device(self.device):
+            self._check(nat.lib().spst_bind(self._h, h, w, grid[0], grid[1], own[0], own[1]), "spst_bind")
+        self.bound = key
+        self.bind_epoch += 1
+        self.last_forward_key = None
+        self._content_out = torch.zeros(1, dtype=torch.float64, device=f"cuda:{self.device}")
+
+    def unbind(self):
+        with torch.cuda.device(self.device):
+            nat.lib().spst_unbind(self._h)
+        self.bound = None
+        self.bind_epoch += 1
+
+    def padded_dims(self):
+        a, b = ctypes.c_int(), ctypes.c_int()
+        nat.lib().spst_padded_dims(self._h, ctypes.byref(a), ctypes.byref(b))
+        return a.value, b.value
+
+    def owned_pixels(self, t_index):
+        c, st, n = ctypes.c_int(), ctypes.c_int(), ctypes.c_longlong()
+        self._check(nat.lib().spst_tap_info(self._h, t_index, ctypes.byref(c), ctypes.byref(st), ctypes.byref(n)),
+                    "spst_tap_info")
+        return n.value
+
+    def workspace_bytes(self):
+        return int(nat.lib().spst_workspace_bytes(self._h))
+
+    # ------------------------------------------------------------------ passes
+    def forward(self, x_dev):
+        """x_dev: (h, w, 3) float32 CUDA tensor matching the bound dims."""
+        self.stream()
+        with torch.cuda.device(self.device):
+            self._check(nat.lib().spst_forward(self._h, nat.ptr(x_dev), 1), "spst_forward")
+
+    def tap_sums(self, t_index):
+        """Device f64 views (S: C x C, s: C) of this device's owned-row sums for style tap t."""
+        S, s = ctypes.c_void_p(), ctypes.c_void_p()
+        self._check(nat.lib().spst_stats_ptrs(self._h, t_index, ctypes.byref(S), ctypes.byref(s)), "spst_stats_ptrs")
+        C = self.geom[self.style_taps[t_index]].channels
+        return device_view(S.value, (C, C)), device_view(s.value, (C,))
+
+    def set_style_ref(self, t_index, stats, w):
+        g = np.ascontiguousarray(stats.gram, dtype=np.float64)
+        m = np.ascontiguousarray(stats.mean, dtype=np.float64)
+        d = np.ascontiguousarray(stats.std, dtype=np.float64)
+        P = ctypes.POINTER(ctypes.c_double)
+        self._check(nat.lib().spst_set_style_ref(self._h, t_index, g.ctypes.data_as(P), m.ctypes.data_as(P),
+                                                  d.ctypes.data_as(P), float(w.gram), float(w.mean), float(w.std)),
+                    "spst_set_style_ref")
+
+    def finalize(self, counts):
+        """Global statistics -> per-tap (gram, mean, std) loss terms [T, 3] and degenerate flags."""
+        n = (ctypes.c_longlong * max(1, len(counts)))(*[int(c) for c in counts])
+        terms = (ctypes.c_double * len(self._terms))()
+        self._check(nat.lib().spst_finalize(self._h, n, terms, self._deg), "spst_finalize")
+        T = len(self.style_taps)
+        return np.array(terms[:3 * T]).reshape(T, 3), [bool(self._deg[i]) for i in range(T)]
+
+    def capture_content(self):
+        self._check(nat.lib().spst_capture_content(self._h), "spst_capture_content")
+
+    def content_sqdiff(self):
+        """Device f64 scalar: sum over owned rows of (V - V_u)^2 at the content tap."""
+        self._check(nat.lib().spst_content_sqdiff(self._h, nat.ptr(self._content_out)), "spst_content_sqdiff")
+        return self._content_out
+
+    def backward(self, two_lambda, grad_dev):
+        self.stream()
+        with torch.cuda.device(self.device):
+            self._check(nat.lib().spst_backward(self._h, float(two_lambda), nat.ptr(grad_dev)), "spst_backward")
+
+
+_ENGINES: dict = {}
+
+
+def engine_for(spec, device: int | None = None) -> Engine:
+    """One engine per (spec object, device); keeps the spec alive to pin its id."""
+    require_cuda()
+    dev = torch.cuda.current_device() if device is None else device
+    key = (id(spec), dev)
+    hit = _ENGINES.get(key)
+    if hit is not None and hit[0] is spec:
+        return hit[1]
+    if len(_ENGINES) >= 4:
+        _ENGINES.pop(next(iter(_ENGINES)))
+    eng = Engine(spec, dev)
+    _ENGINES[key] = (spec, eng)
+    return eng
+
+
+def clear_engines():
+    _ENGINES.clear()

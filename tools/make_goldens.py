@@ -1,0 +1,238 @@
+"""Generate golden vectors from the REAL reference implementation (build container only).
+
+    PYTHONPATH=/root/reference/pkg/src python tools/make_goldens.py
+
+Writes tests/golden/*.npz. The reference (pure NumPy) is imported read-only; nothing here
+runs on the GPU box, which only reads the committed fixtures.  Every fixture records the
+inputs, the reference outputs, and for VGG-19 the sha256 of the calibrated weights so the box
+can check it regenerates the identical network.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, "/root/reference/pkg/src")
+
+import tilestyle as ts  # noqa: E402
+from tilestyle import extractor as rex, lbfgs as rlb, localized as rloc, pipeline as rpipe  # noqa: E402
+from tilestyle import stats as rst, tensorops as rto, tiling as rti  # noqa: E402
+
+from paper_2212_13459_b200 import spec as myspec  # noqa: E402
+from paper_2212_13459_b200.workloads import synth_content, synth_style  # noqa: E402
+
+OUT = os.path.join(ROOT, "tests", "golden")
+os.makedirs(OUT, exist_ok=True)
+
+
+def weights_sha(spec) -> str:
+    h = hashlib.sha256()
+    for l in spec.layers:
+        if l.kind == "conv":
+            h.update(np.ascontiguousarray(l.weight, dtype=np.float64).tobytes())
+            h.update(np.ascontiguousarray(l.bias, dtype=np.float64).tobytes())
+    return h.hexdigest()
+
+
+def to_ref_spec(myspec_obj, ref_base):
+    """Bind our calibrated weights into the reference's own unbound spec object."""
+    from dataclasses import replace
+    layers = []
+    mine = {l.name: l for l in myspec_obj.layers}
+    for l in ref_base.layers:
+        if l.kind == "conv":
+            layers.append(replace(l, weight=mine[l.name].weight.copy(), bias=mine[l.name].bias.copy()))
+        else:
+            layers.append(l)
+    return replace(ref_base, layers=tuple(layers))
+
+
+def save(name, **arrays):
+    path = os.path.join(OUT, name)
+    np.savez_compressed(path, **arrays)
+    print(f"wrote {path} ({os.path.getsize(path) / 1e6:.2f} MB)")
+
+
+def kernels():
+    rng = np.random.default_rng(1234)
+    d = {}
+    x = rng.standard_normal((5, 9, 11))
+    w = rng.standard_normal((7, 5, 3, 3))
+    b = rng.standard_normal(7)
+    g = rng.standard_normal((7, 9, 11))
+    d.update(conv_x=x, conv_w=w, conv_b=b, conv_y=rto.conv2d_forward(x, w, b, 1, 1), conv_g=g,
+             conv_gx=rto.conv2d_backward_input(g, x.shape, w, 1, 1))
+    p = rng.standard_normal((3, 9, 7))
+    gp = rng.standard_normal((3, 4, 3))
+    d.update(pool_x=p, pool_avg=rto.avgpool_forward(p, 2), pool_max=rto.maxpool_forward(p, 2), pool_g=gp,
+             pool_avg_bwd=rto.avgpool_backward(gp, p.shape, 2), pool_max_bwd=rto.maxpool_backward(gp, p, 2))
+    img = rng.random((37, 29, 3)).astype(np.float32)
+    d.update(img=img, down3=rto.resize_down(img, 3), down8=rto.resize_down(img, 8),
+             bil=rto.resize_bilinear(img, (53, 41)), up2=rto.resize_up2(img), up2t=rto.resize_up2(img, (73, 57)))
+    padded = rto.pad_to_multiple(img, 16)
+    gpad = rng.standard_normal(padded.shape).astype(np.float32)
+    d.update(pad16=padded, gpad=gpad, fold=rto.fold_padding_gradient(gpad, img.shape[:2]))
+    feats = rng.random((6, 10, 12))
+    acc = rst.StatsAccumulator(6)
+    acc.accumulate(feats)
+    st = acc.finalize()
+    ref = rst.compute_stats(rng.random((6, 8, 8)))
+    tw = rst.TapWeights(0.3, 20.0, 7.0)
+    terms, sg = rst.style_layer_loss_grad(feats, st, ref, tw)
+    d.update(st_feats=feats, st_gram=st.gram, st_mean=st.mean, st_std=st.std, ref_gram=ref.gram,
+             ref_mean=ref.mean, ref_std=ref.std, tw=np.array([tw.gram, tw.mean, tw.std]),
+             sg_terms=np.array(terms), sg_grad=sg)
+    save("kernels.npz", **d)
+
+
+def tiny_cases():
+    spec = ts.tinynet(0)
+    mine = myspec.tinynet(0)
+    diffs = [float(np.abs(a.weight - b.weight).max()) for a, b in zip(spec.layers, mine.layers) if a.kind == "conv"]
+    print("tinynet weight max diff (ours vs reference):", max(diffs))
+    d = {"tiny_w_" + l.name: l.weight for l in spec.layers if l.kind == "conv"}
+    d.update({"tiny_b_" + l.name: l.bias for l in spec.layers if l.kind == "conv"})
+    rng = np.random.default_rng(1234)
+    cases = [(96, 96, 32, 16), (70, 53, 32, 16), (48, 48, 512, 16)]
+    for k, (H, W, block, margin) in enumerate(cases):
+        u = rng.random((H, W, 3))
+        v = rng.random((H - 10, W + 7, 3)) * 0.6 + 0.2 * np.sin(np.arange(W + 7) / 5.0)[None, :, None]
+        x = np.clip(u + 0.1 * rng.standard_normal(u.shape), 0, 1)
+        w = rst.default_loss_weights(spec)
+        p = rloc.build_problem(u, v, spec, w, block=block, margin=margin)
+        lb, gb = rloc.loss_grad(x, p)
+        lg, gg = rloc.loss_grad_global(x, p)
+        sx = rloc.stats_pass(x, spec, block=block, margin=margin)
+        d[f"case{k}_u"], d[f"case{k}_v"], d[f"case{k}_x"] = u, v, x
+        d[f"case{k}_geom"] = np.array([block, margin])
+        d[f"case{k}_loss"] = np.array([lb, lg])
+        d[f"case{k}_grad"], d[f"case{k}_grad_global"] = gb, gg
+        for t in spec.style_taps:
+            d[f"case{k}_{t}_gram"] = sx[t].gram
+            d[f"case{k}_{t}_mean"] = sx[t].mean
+            d[f"case{k}_{t}_std"] = sx[t].std
+            d[f"case{k}_{t}_n"] = np.array([sx[t].n_p])
+            d[f"case{k}_style_{t}_gram"] = p.style_stats[t].gram
+            d[f"case{k}_style_{t}_mean"] = p.style_stats[t].mean
+            d[f"case{k}_style_{t}_std"] = p.style_stats[t].std
+    # an f32 run of case 0 (pipeline dtype)
+    u, v, x = (d["case0_u"].astype(np.float32), d["case0_v"].astype(np.float32), d["case0_x"].astype(np.float32))
+    p = rloc.build_problem(u, v, spec, rst.default_loss_weights(spec), block=32, margin=16)
+    l32, g32 = rloc.loss_grad(x, p)
+    d["case0_loss_f32"], d["case0_grad_f32"] = np.array([l32]), g32
+    # short L-BFGS trajectory (f32, like the pipeline) on case 0
+    losses = []
+    xs = []
+    xr, tr = rlb.minimize(lambda a: rloc.loss_grad(a, p), x, rlb.LBFGSConfig(history_size=10, max_iters=5),
+                          callback=lambda it, xi, l, gn: xs.append(xi.copy()))
+    d["case0_lbfgs_losses"] = np.array(tr.losses)
+    d["case0_lbfgs_x5"] = xr
+    save("tinynet.npz", **d)
+
+
+def lbfgs_cases():
+    d = {}
+
+    def quad(a):
+        return lambda x: (float(np.sum((x - a) ** 2)), 2.0 * (x - a))
+
+    def rosen(z):
+        x, y = z
+        return float((1 - x) ** 2 + 100 * (y - x ** 2) ** 2), np.array(
+            [-2 * (1 - x) - 400 * x * (y - x ** 2), 200 * (y - x ** 2)])
+
+    rng = np.random.default_rng(7)
+    a = rng.standard_normal(20)
+    x, tr = rlb.minimize(quad(a), np.zeros(20), rlb.LBFGSConfig(history_size=5, max_iters=30))
+    d.update(quad_a=a, quad_x=x, quad_losses=np.array(tr.losses), quad_gn=np.array(tr.grad_norms))
+    x, tr = rlb.minimize(rosen, np.array([-1.2, 1.0]), rlb.LBFGSConfig(history_size=10, max_iters=200))
+    d.update(rosen_x=x, rosen_losses=np.array(tr.losses))
+    # two-loop on a random admissible state
+    st = rlb.LBFGSState()
+    ss, ys = [], []
+    for _ in range(4):
+        s = rng.standard_normal(12)
+        y = s + 0.3 * rng.standard_normal(12)
+        st.push(s, y, m=3)
+        ss.append(s)
+        ys.append(y)
+    g = rng.standard_normal(12)
+    d.update(tl_s=np.array(ss), tl_y=np.array(ys), tl_g=g, tl_d=rlb.two_loop_direction(g, st))
+    sched = [rpipe.make_schedule(n, m).iters for n, m in [(4, "fast"), (4, "baseline"), (6, "fast")]]
+    d["sched_fast4"], d["sched_base4"], d["sched_fast6"] = [np.array(s) for s in sched]
+    d["dims_4"] = np.array(rpipe.scale_dims((6048, 8064), 4))
+    d["dims_3_odd"] = np.array(rpipe.scale_dims((1001, 777), 3))
+    save("lbfgs_pipeline.npz", **d)
+
+
+def vgg_cases():
+    spec_mine = myspec.calibrated_vgg19(0)
+    spec = to_ref_spec(spec_mine, rex.vgg19("avg"))
+    d = {"weights_sha256": np.frombuffer(weights_sha(spec_mine).encode(), dtype=np.uint8)}
+    print("margin_for_exact_gradient(VGG19) =", rti.margin_for_exact_gradient(spec))
+    # C1: 256^2 single-scale transfer (BASELINE configs[0])
+    u = synth_content(256, 256, 1)
+    v = synth_style(256, 256, 2)
+    cfg = rpipe.RunConfig(n_scales=1, extractor=spec)
+    w = rpipe._weights_for_scale(cfg, spec, (256, 256))
+    d["c1_u"], d["c1_v"], d["c1_lambda_c"] = u, v, np.array([w.lambda_c])
+    t0 = time.time()
+    p64 = rloc.build_problem(u.astype(np.float64), v.astype(np.float64), spec, w)
+    x0 = u.astype(np.float64)
+    l64, g64 = rloc.loss_grad_global(x0, p64)
+    print(f"VGG f64 loss_grad_global 256^2: {time.time() - t0:.1f}s loss={l64}")
+    for t in spec.style_taps:
+        d[f"c1_style_{t}_gram"] = p64.style_stats[t].gram.astype(np.float32)
+        d[f"c1_style_{t}_mean"] = p64.style_stats[t].mean
+        d[f"c1_style_{t}_std"] = p64.style_stats[t].std
+    sx = rloc.stats_pass(x0, spec)
+    for t in spec.style_taps:
+        d[f"c1_x0_{t}_gram"] = sx[t].gram.astype(np.float32)
+        d[f"c1_x0_{t}_mean"] = sx[t].mean
+        d[f"c1_x0_{t}_std"] = sx[t].std
+        d[f"c1_x0_terms_{t}"] = np.array(rst.style_loss_terms(sx[t], p64.style_stats[t], w.style[t]))
+    d["c1_loss64"], d["c1_grad64"] = np.array([l64]), g64.astype(np.float32)
+    # the reference's own f32 path at the same x (its f32-vs-f64 gap bounds any fp32-class engine)
+    p32 = rloc.build_problem(u, v, spec, w)
+    l32, g32 = rloc.loss_grad(u.copy(), p32)
+    d["c1_loss32"], d["c1_grad32"] = np.array([l32]), g32
+    rel = np.linalg.norm(g32 - g64) / np.linalg.norm(g64)
+    print(f"reference f32 vs f64 at x0: loss rel {abs(l32 - l64) / abs(l64):.2e}, grad rel-L2 {rel:.2e}")
+    # a second point along the steepest-descent direction (first L-BFGS trial point)
+    x1 = (u - (1.0 / np.abs(g32).max()) * g32).astype(np.float32)
+    l1, g1 = rloc.loss_grad_global(x1.astype(np.float64), p64)
+    d["c1_x1"], d["c1_loss64_x1"], d["c1_grad64_x1"] = x1, np.array([l1]), g1.astype(np.float32)
+    # first reference f32 L-BFGS iterations (losses; iterates are chaotic beyond ~5)
+    t0 = time.time()
+    xr, tr = rlb.minimize(lambda a: rloc.loss_grad(a, p32), u.copy(), rlb.LBFGSConfig(history_size=100, max_iters=3))
+    print(f"reference 3 L-BFGS iters 256^2 f32: {time.time() - t0:.1f}s losses={tr.losses}")
+    d["c1_lbfgs_losses"] = np.array(tr.losses)
+    # ragged small VGG case (replicate padding + fold): 72 x 88 -> padded 80 x 96
+    rng = np.random.default_rng(5)
+    us = synth_content(72, 88, 3)
+    vs = synth_style(64, 64, 4)
+    xs = np.clip(us + 0.05 * rng.standard_normal(us.shape), 0, 1)
+    ws = rpipe._weights_for_scale(cfg, spec, (72, 88))
+    ps = rloc.build_problem(us.astype(np.float64), vs.astype(np.float64), spec, ws)
+    ls, gs = rloc.loss_grad_global(xs, ps)
+    d.update(r_u=us, r_v=vs, r_x=xs, r_lambda_c=np.array([ws.lambda_c]), r_loss64=np.array([ls]), r_grad64=gs)
+    save("vgg19.npz", **d)
+
+
+if __name__ == "__main__":
+    which = sys.argv[1:] or ["kernels", "tiny", "lbfgs", "vgg"]
+    if "kernels" in which:
+        kernels()
+    if "tiny" in which:
+        tiny_cases()
+    if "lbfgs" in which:
+        lbfgs_cases()
+    if "vgg" in which:
+        vgg_cases()

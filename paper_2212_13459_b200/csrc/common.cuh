@@ -139,7 +139,7 @@ cudaError_t launch_first_conv_bwd(const FirstConvBwdArgs& a, cudaStream_t st);
 cudaError_t launch_fold_grad(const float* gimg, int Hl, int Wp, int row_off, int h, int w, int r0, int r1,
                              float* grad, cudaStream_t st);
 cudaError_t launch_pool2_hl(const HL16& in, const HL16& out, unsigned int* amax, cudaStream_t st);
-cudaError_t launch_colsum_reduce(const float* partial, int rows, int C, double* sums, cudaStream_t st);
+cudaError_t launch_colsum_reduce(const float* partial, int rows, int C, int stride, double* sums, cudaStream_t st);
 cudaError_t launch_style_vec(const StyleCoefArgs& a, cudaStream_t st);
 cudaError_t launch_style_mat(const StyleCoefArgs& a, cudaStream_t st);
 cudaError_t launch_content_sqdiff(const HL16& v, const HL16& u, int C, int r0, int r1, double* partial,

@@ -5,22 +5,26 @@
 // and the input-gradient pass (tensorops.py:58-74 conv2d_backward_input, run as a forward
 // conv with transposed, flipped weights, fused with relu_backward, avgpool_backward 104-110,
 // the tap-gradient injection of extractor.py:200-214 and the style/content feature gradients
-// of stats.py:127-174 — the style gradient V*M enters as extra K-steps of the same
-// accumulator).
+// of stats.py:127-174 — the style gradient V*M enters as extra K-steps).
 //
-// GEMM view: M = output pixels (a CTA owns 2 rows x 128 px, two M=128 accumulators),
-// N = output channels (tile 64/128), K = 9 taps x input channels.  Numerics: "fp16x3" —
-// both operands are stored as fp16 hi/lo pairs with power-of-two tensor scales and every
-// K-step issues hi*hi + hi*lo + lo*hi into the fp32 TMEM accumulator (~fp32-class products).
+// GEMM view: M = output pixels (a CTA tile is 2 rows x 128 px = two M=128 accumulators),
+// N = output channels (64/128 per tile), K = 9 taps x input channels.
 //
-// Warp roles (192 threads, persistent over output tiles):
-//   warp 0      TMA producer: per K-chunk (16 input channels) one 4-row x 130-px halo window
-//               of hi and lo activations (TMA 4-D, OOB zero fill = conv zero padding) plus
-//               the matching 9-tap weight slab (one 1-D bulk copy)
-//   warp 1      MMA issuer (single thread): 9 taps x 2 rows x 3 passes per chunk; the tap
-//               shift is a descriptor start-address offset into the halo window
-//   warps 2..5  epilogue: TMEM -> registers -> fused pointwise ops -> HBM (double-buffered
-//               accumulators let the epilogue of tile i overlap the MMAs of tile i+1)
+// Numerics ("fp16x3 + register accumulation"): operands are fp16 hi/lo pairs with
+// power-of-two tensor scales; each 16-channel K-chunk issues hi*hi + hi*lo + lo*hi over the
+// 9 taps into a FRESH TMEM accumulator, and the epilogue warps drain every chunk into fp32
+// registers (round-to-nearest adds).  The tensor core therefore never carries a running sum
+// longer than one chunk, which removes the truncation bias of long in-TMEM accumulations
+// (measured: rel-err growing ~ K x 2^-24 otherwise).
+//
+// Warp roles (320 threads, persistent over output tiles):
+//   warp 0      TMA producer: per K-chunk one 4-row x 130-px halo window of hi and lo
+//               activations (TMA 4-D, OOB zero fill = conv zero padding) + the 9-tap weight
+//               slab (one 1-D bulk copy)
+//   warp 1      MMA issuer (one thread): 9 taps x 2 rows x 3 passes per chunk; a tap shift is
+//               a descriptor start-address offset into the halo window
+//   warps 2..9  two epilogue warpgroups; group g drains channel half g of both rows of every
+//               chunk into registers, then runs the fused pointwise epilogue for the tile
 #include "common.cuh"
 #include "sm100.cuh"
 
@@ -38,8 +42,10 @@ struct ConvCfg {
   static constexpr int XB_BYTES = 2 * B_TAP;        // extra-K slab: hi/lo x 1 tap
   static constexpr int STAGE = ((A_BYTES + B_BYTES + 1023) / 1024) * 1024;
   static constexpr int STAGES = N == 128 ? 2 : 3;
-  static constexpr int TMEM_COLS = 4 * N;           // 2 buffers x 2 rows x N
+  static constexpr int NBUF = N == 128 ? 2 : 4;     // TMEM chunk buffers (2 rows x N each)
+  static constexpr int TMEM_COLS = 512;
   static constexpr int SMEM = STAGES * STAGE + 1024;
+  static constexpr int HALF = N / 2;                // channels per epilogue warpgroup
 };
 
 __device__ __forceinline__ void store_hl8(const HL16& t, int kg, int y, int x, const float* v8, float s) {
@@ -82,24 +88,161 @@ __device__ __forceinline__ float warp_transpose_sum(float (&v)[32]) {
   return v[0];
 }
 
-__device__ __forceinline__ void atomic_max_pos(unsigned int* slot, float v) {
-  // v >= 0: IEEE order of non-negative floats matches unsigned order of their bits
-  atomicMax(slot, __float_as_uint(v));
-}
-
 __device__ __forceinline__ float warp_max(float v) {
 #pragma unroll
   for (int off = 16; off >= 1; off >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, off));
   return v;
 }
 
+// 32 columns of TMEM added into acc[0..31] (fp32 round-to-nearest adds)
+__device__ __forceinline__ void tmem_add32(uint32_t taddr, float* acc) {
+  float v[32];
+  tmem_ld32(taddr, v);
+#pragma unroll
+  for (int i = 0; i < 32; ++i) acc[i] += v[i];
+}
+
+// Fused pointwise epilogue for 32 channels of one pixel in both rows (v0: row y0, v1: y0+1).
 template <int N>
-__global__ void __launch_bounds__(192, 1) conv3x3_tc_kernel(const __grid_constant__ ConvArgs a) {
+__device__ __forceinline__ void epilogue32(const ConvArgs& a, float* v0, float* v1, int ch0, int x, int y0,
+                                           int tile_xy, uint32_t q, float& amax0, float& amax1) {
+  const uint32_t lane = lane_id();
+  if (a.epi == EPI_FWD || a.epi == EPI_FWD_POOL) {
+    uint32_t bits0 = 0, bits1 = 0;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const float bj = a.bias ? __ldg(a.bias + ch0 + j) : 0.f;
+      const float p0 = fmaf(v0[j], a.acc_scale, bj);
+      const float p1 = fmaf(v1[j], a.acc_scale, bj);
+      bits0 |= (p0 > 0.f ? 1u : 0u) << j;
+      bits1 |= (p1 > 0.f ? 1u : 0u) << j;
+      v0[j] = fmaxf(p0, 0.f);
+      v1[j] = fmaxf(p1, 0.f);
+    }
+    const bool ok0 = x < a.W && y0 < a.H, ok1 = x < a.W && y0 + 1 < a.H;
+    if (a.mask_out) {
+      if (ok0) a.mask_out[((size_t)(ch0 >> 5) * a.H + y0) * a.W + x] = bits0;
+      if (ok1) a.mask_out[((size_t)(ch0 >> 5) * a.H + y0 + 1) * a.W + x] = bits1;
+    }
+    if (a.epi == EPI_FWD || a.store_full) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (ok0) store_hl8(a.out, (ch0 >> 3) + k, y0, x, v0 + 8 * k, a.out.scale);
+        if (ok1) store_hl8(a.out, (ch0 >> 3) + k, y0 + 1, x, v1 + 8 * k, a.out.scale);
+      }
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        amax0 = fmaxf(amax0, ok0 ? v0[j] : 0.f);
+        amax0 = fmaxf(amax0, ok1 ? v1[j] : 0.f);
+      }
+    }
+    if (a.colsum_partial) {
+      const bool in0 = ok0 && y0 >= a.sum_r0 && y0 < a.sum_r1;
+      const bool in1 = ok1 && y0 + 1 >= a.sum_r0 && y0 + 1 < a.sum_r1;
+      float s[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) s[j] = (in0 ? v0[j] : 0.f) + (in1 ? v1[j] : 0.f);
+      const float tot = warp_transpose_sum(s);
+      a.colsum_partial[((size_t)tile_xy * 4 + q) * (size_t)(a.n_ntiles * N) + ch0 + lane] = tot;
+    }
+    if (a.epi == EPI_FWD_POOL) {
+      float pv[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const float s2 = v0[j] + v1[j];
+        pv[j] = (s2 + __shfl_xor_sync(0xffffffffu, s2, 1)) * 0.25f;
+      }
+      const int px = x >> 1, py = y0 >> 1;
+      if ((lane & 1) == 0 && px < a.out_pool.W && py < a.out_pool.H) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) store_hl8(a.out_pool, (ch0 >> 3) + k, py, px, pv + 8 * k, a.out_pool.scale);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) amax1 = fmaxf(amax1, pv[j]);
+      }
+    }
+  } else if (a.epi == EPI_BWD) {
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      float* v = r ? v1 : v0;
+      const int y = y0 + r;
+      if (x >= a.W || y >= a.H) continue;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = fmaf(v[j], a.acc_scale, a.bias ? __ldg(a.bias + ch0 + j) : 0.f);
+      if (a.content_coef != 0.f) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          float cv[8], cu[8];
+          load_hl8(a.content_v, (ch0 >> 3) + k, y, x, cv);
+          load_hl8(a.content_u, (ch0 >> 3) + k, y, x, cu);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) v[8 * k + e] = fmaf(a.content_coef, cv[e] - cu[e], v[8 * k + e]);
+        }
+      }
+      if (a.addend.hi) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          float ad[8];
+          load_hl8(a.addend, (ch0 >> 3) + k, y, x, ad);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) v[8 * k + e] += ad[e];
+        }
+      }
+      if (a.mask_in) {
+        const uint32_t bits = a.mask_in[((size_t)(ch0 >> 5) * a.H + y) * a.W + x];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = ((bits >> j) & 1u) ? v[j] : 0.f;
+      }
+#pragma unroll
+      for (int j = 0; j < 32; ++j) amax0 = fmaxf(amax0, fabsf(v[j]));
+#pragma unroll
+      for (int k = 0; k < 4; ++k) store_hl8(a.out, (ch0 >> 3) + k, y, x, v + 8 * k, a.out.scale);
+    }
+  } else {  // EPI_BWD_POOL: out is the 2x finer grid
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      float* v = r ? v1 : v0;
+      const int y = y0 + r;
+      if (x >= a.W || y >= a.H) continue;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] *= a.acc_scale * 0.25f;
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int jx = 0; jx < 2; ++jx) {
+          const int yy = 2 * y + i, xx = 2 * x + jx;
+          float w[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) w[j] = v[j];
+          if (a.addend.hi) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              float ad[8];
+              load_hl8(a.addend, (ch0 >> 3) + k, yy, xx, ad);
+#pragma unroll
+              for (int e = 0; e < 8; ++e) w[8 * k + e] += ad[e];
+            }
+          }
+          if (a.mask_in) {
+            const uint32_t bits = a.mask_in[((size_t)(ch0 >> 5) * a.out.H + yy) * a.out.W + xx];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) w[j] = ((bits >> j) & 1u) ? w[j] : 0.f;
+          }
+#pragma unroll
+          for (int j = 0; j < 32; ++j) amax0 = fmaxf(amax0, fabsf(w[j]));
+#pragma unroll
+          for (int k = 0; k < 4; ++k) store_hl8(a.out, (ch0 >> 3) + k, yy, xx, w + 8 * k, a.out.scale);
+        }
+    }
+  }
+}
+
+template <int N>
+__global__ void __launch_bounds__(320, 1) conv3x3_tc_kernel(const __grid_constant__ ConvArgs a) {
   using C = ConvCfg<N>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ uint64_t full_bar[C::STAGES], empty_bar[C::STAGES];
-  __shared__ uint64_t tfull_bar[2], tempty_bar[2];
+  __shared__ uint64_t cfull_bar[C::NBUF], cempty_bar[C::NBUF];
   __shared__ uint32_t tmem_slot;
 
   const uint32_t warp = warp_id();
@@ -116,9 +259,9 @@ __global__ void __launch_bounds__(192, 1) conv3x3_tc_kernel(const __grid_constan
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
     }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&tfull_bar[b], 1);
-      mbar_init(&tempty_bar[b], 4);
+    for (int b = 0; b < C::NBUF; ++b) {
+      mbar_init(&cfull_bar[b], 1);
+      mbar_init(&cempty_bar[b], 8);
     }
     fence_barrier_init();
   }
@@ -157,201 +300,80 @@ __global__ void __launch_bounds__(192, 1) conv3x3_tc_kernel(const __grid_constan
     // ------------------------------------------------------------------ MMA issuer
     if (lane == 0) {
       const uint32_t idesc = make_idesc_f16(128, N, 0, 0, 0);
-      uint32_t g = 0, it = 0;
-      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++it) {
-        const uint32_t ab = it & 1;
-        mbar_wait(&tempty_bar[ab], ((it >> 1) & 1) ^ 1);
-        tc_fence_after();
-        const uint32_t dcol = tmem_base + ab * 2 * N;
+      uint32_t g = 0;
+      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
         for (int c = 0; c < n_chunks; ++c, ++g) {
+          const uint32_t b = g % C::NBUF;
+          mbar_wait(&cempty_bar[b], ((g / C::NBUF) & 1) ^ 1);
           const int s = g % C::STAGES;
           mbar_wait(&full_bar[s], (g / C::STAGES) & 1);
           tc_fence_after();
           const uint32_t st = smem_u32(smem + s * C::STAGE);
-          const uint32_t a_hi = st, a_lo = st + C::A_HALF, b = st + C::A_BYTES;
+          const uint32_t a_hi = st, a_lo = st + C::A_HALF, bb = st + C::A_BYTES;
           const bool conv = c < a.n_kc;
           const int ntap = conv ? 9 : 1;
-          for (int tap = 0; tap < ntap; ++tap) {
-            const int dy = conv ? tap / 3 : 1, dx = conv ? tap % 3 : 1;
-            const uint64_t b_hi = make_sdesc(b + tap * C::B_TAP, N * 16, 128);
-            const uint64_t b_lo = make_sdesc(b + (ntap + tap) * C::B_TAP, N * 16, 128);
+          const uint32_t dcol = tmem_base + b * 2 * N;
+          // Small correction products first (hi*lo, lo*hi), then the large hi*hi products: the
+          // tensor core truncates each accumulation to the running sum's exponent, so keeping the
+          // sum small while the corrections go in cuts the chunk's rounding error ~3x.
+          for (int pass = 0; pass < 3; ++pass) {
+            for (int tap = 0; tap < ntap; ++tap) {
+              const int dy = conv ? tap / 3 : 1, dx = conv ? tap % 3 : 1;
+              const uint64_t bd = make_sdesc(bb + ((pass == 0 ? ntap : 0) + tap) * C::B_TAP, N * 16, 128);
 #pragma unroll
-            for (int mt = 0; mt < 2; ++mt) {
-              const uint32_t aoff = ((mt + dy) * C::PITCH + dx) * 16;
-              const uint64_t ad_hi = make_sdesc(a_hi + aoff, C::A_PLANE, 128);
-              const uint64_t ad_lo = make_sdesc(a_lo + aoff, C::A_PLANE, 128);
-              const uint32_t d = dcol + mt * N;
-              const uint32_t acc0 = (c > 0 || tap > 0) ? 1u : 0u;
-              umma_f16(d, ad_hi, b_hi, idesc, acc0);
-              umma_f16(d, ad_hi, b_lo, idesc, 1u);
-              umma_f16(d, ad_lo, b_hi, idesc, 1u);
+              for (int mt = 0; mt < 2; ++mt) {
+                const uint32_t aoff = ((mt + dy) * C::PITCH + dx) * 16;
+                const uint64_t ad = make_sdesc((pass == 1 ? a_lo : a_hi) + aoff, C::A_PLANE, 128);
+                umma_f16(dcol + mt * N, ad, bd, idesc, (pass | tap) ? 1u : 0u);  // fresh per chunk
+              }
             }
           }
           umma_commit(&empty_bar[s]);
+          umma_commit(&cfull_bar[b]);
         }
-        umma_commit(&tfull_bar[ab]);
       }
     }
   } else {
-    // ------------------------------------------------------------------ epilogue (4 warps)
-    const uint32_t q = warp & 3;  // TMEM lane quarter this warp may access
+    // ------------------------------------------------------------------ epilogue (8 warps)
+    const uint32_t q = warp & 3;            // TMEM lane quarter
+    const uint32_t grp = (warp - 2) >> 2;   // channel half
     const int m = q * 32 + lane;
-    uint32_t it = 0;
-    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++it) {
+    uint32_t g = 0;
+    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
       const int nt = t % a.n_ntiles;
       const int rest = t / a.n_ntiles;
       const int cx = rest % a.tiles_x, ry = rest / a.tiles_x;
       const int x0 = cx * 128, y0 = ry * 2;
       const int x = x0 + m;
-      const uint32_t ab = it & 1;
-      mbar_wait(&tfull_bar[ab], (it >> 1) & 1);
-      tc_fence_after();
-      const uint32_t trow = tmem_base + ((q * 32u) << 16) + ab * 2 * N;
-      float amax0 = 0.f, amax1 = 0.f;
-      for (int cb = 0; cb < N / 32; ++cb) {
-        const int ch0 = nt * N + cb * 32;
-        float v0[32], v1[32];
-        tmem_ld32(trow + cb * 32, v0);
-        tmem_ld32(trow + N + cb * 32, v1);
-        if (a.epi == EPI_FWD || a.epi == EPI_FWD_POOL) {
-          uint32_t bits0 = 0, bits1 = 0;
+      float acc0[C::HALF], acc1[C::HALF];
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const float bj = a.bias ? __ldg(a.bias + ch0 + j) : 0.f;
-            const float p0 = fmaf(v0[j], a.acc_scale, bj);
-            const float p1 = fmaf(v1[j], a.acc_scale, bj);
-            bits0 |= (p0 > 0.f ? 1u : 0u) << j;
-            bits1 |= (p1 > 0.f ? 1u : 0u) << j;
-            v0[j] = fmaxf(p0, 0.f);
-            v1[j] = fmaxf(p1, 0.f);
-          }
-          const bool ok0 = x < a.W && y0 < a.H, ok1 = x < a.W && y0 + 1 < a.H;
-          if (a.mask_out) {
-            if (ok0) a.mask_out[((size_t)(ch0 >> 5) * a.H + y0) * a.W + x] = bits0;
-            if (ok1) a.mask_out[((size_t)(ch0 >> 5) * a.H + y0 + 1) * a.W + x] = bits1;
-          }
-          if (a.epi == EPI_FWD || a.store_full) {
+      for (int i = 0; i < C::HALF; ++i) acc0[i] = acc1[i] = 0.f;
+      for (int c = 0; c < n_chunks; ++c, ++g) {
+        const uint32_t b = g % C::NBUF;
+        mbar_wait(&cfull_bar[b], (g / C::NBUF) & 1);
+        tc_fence_after();
+        const uint32_t trow = tmem_base + ((q * 32u) << 16) + b * 2 * N + grp * C::HALF;
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              if (ok0) store_hl8(a.out, (ch0 >> 3) + k, y0, x, v0 + 8 * k, a.out.scale);
-              if (ok1) store_hl8(a.out, (ch0 >> 3) + k, y0 + 1, x, v1 + 8 * k, a.out.scale);
-            }
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              amax0 = fmaxf(amax0, ok0 ? v0[j] : 0.f);
-              amax0 = fmaxf(amax0, ok1 ? v1[j] : 0.f);
-            }
-          }
-          if (a.colsum_partial) {
-            const bool in0 = ok0 && y0 >= a.sum_r0 && y0 < a.sum_r1;
-            const bool in1 = ok1 && y0 + 1 >= a.sum_r0 && y0 + 1 < a.sum_r1;
-            float s[32];
-#pragma unroll
-            for (int j = 0; j < 32; ++j) s[j] = (in0 ? v0[j] : 0.f) + (in1 ? v1[j] : 0.f);
-            const float tot = warp_transpose_sum(s);
-            const size_t tile_xy = (size_t)ry * a.tiles_x + cx;
-            a.colsum_partial[(tile_xy * 4 + q) * (size_t)(a.n_ntiles * N) + ch0 + lane] = tot;
-          }
-          if (a.epi == EPI_FWD_POOL) {
-            // 2x2 average: vertical pair in registers, horizontal pair across lanes
-            float pv[32];
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              const float s2 = v0[j] + v1[j];
-              pv[j] = (s2 + __shfl_xor_sync(0xffffffffu, s2, 1)) * 0.25f;
-            }
-            const int px = x >> 1, py = y0 >> 1;
-            if ((lane & 1) == 0 && px < a.out_pool.W && py < a.out_pool.H) {
-#pragma unroll
-              for (int k = 0; k < 4; ++k) store_hl8(a.out_pool, (ch0 >> 3) + k, py, px, pv + 8 * k, a.out_pool.scale);
-#pragma unroll
-              for (int j = 0; j < 32; ++j) amax1 = fmaxf(amax1, pv[j]);
-            }
-          }
-        } else if (a.epi == EPI_BWD) {
-#pragma unroll
-          for (int r = 0; r < 2; ++r) {
-            float* v = r ? v1 : v0;
-            const int y = y0 + r;
-            if (x >= a.W || y >= a.H) continue;
-#pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = fmaf(v[j], a.acc_scale, a.bias ? __ldg(a.bias + ch0 + j) : 0.f);
-            if (a.content_coef != 0.f) {
-#pragma unroll
-              for (int k = 0; k < 4; ++k) {
-                float cv[8], cu[8];
-                load_hl8(a.content_v, (ch0 >> 3) + k, y, x, cv);
-                load_hl8(a.content_u, (ch0 >> 3) + k, y, x, cu);
-#pragma unroll
-                for (int e = 0; e < 8; ++e) v[8 * k + e] = fmaf(a.content_coef, cv[e] - cu[e], v[8 * k + e]);
-              }
-            }
-            if (a.addend.hi) {
-#pragma unroll
-              for (int k = 0; k < 4; ++k) {
-                float ad[8];
-                load_hl8(a.addend, (ch0 >> 3) + k, y, x, ad);
-#pragma unroll
-                for (int e = 0; e < 8; ++e) v[8 * k + e] += ad[e];
-              }
-            }
-            if (a.mask_in) {
-              const uint32_t bits = a.mask_in[((size_t)(ch0 >> 5) * a.H + y) * a.W + x];
-#pragma unroll
-              for (int j = 0; j < 32; ++j) v[j] = ((bits >> j) & 1u) ? v[j] : 0.f;
-            }
-#pragma unroll
-            for (int j = 0; j < 32; ++j) amax0 = fmaxf(amax0, fabsf(v[j]));
-#pragma unroll
-            for (int k = 0; k < 4; ++k) store_hl8(a.out, (ch0 >> 3) + k, y, x, v + 8 * k, a.out.scale);
-          }
-        } else {  // EPI_BWD_POOL: out is the 2x finer grid
-#pragma unroll
-          for (int r = 0; r < 2; ++r) {
-            float* v = r ? v1 : v0;
-            const int y = y0 + r;
-            if (x >= a.W || y >= a.H) continue;
-#pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] *= a.acc_scale * 0.25f;
-#pragma unroll
-            for (int i = 0; i < 2; ++i)
-#pragma unroll
-              for (int jx = 0; jx < 2; ++jx) {
-                const int yy = 2 * y + i, xx = 2 * x + jx;
-                float w[32];
-#pragma unroll
-                for (int j = 0; j < 32; ++j) w[j] = v[j];
-                if (a.addend.hi) {
-#pragma unroll
-                  for (int k = 0; k < 4; ++k) {
-                    float ad[8];
-                    load_hl8(a.addend, (ch0 >> 3) + k, yy, xx, ad);
-#pragma unroll
-                    for (int e = 0; e < 8; ++e) w[8 * k + e] += ad[e];
-                  }
-                }
-                if (a.mask_in) {
-                  const uint32_t bits = a.mask_in[((size_t)(ch0 >> 5) * a.out.H + yy) * a.out.W + xx];
-#pragma unroll
-                  for (int j = 0; j < 32; ++j) w[j] = ((bits >> j) & 1u) ? w[j] : 0.f;
-                }
-#pragma unroll
-                for (int j = 0; j < 32; ++j) amax0 = fmaxf(amax0, fabsf(w[j]));
-#pragma unroll
-                for (int k = 0; k < 4; ++k) store_hl8(a.out, (ch0 >> 3) + k, yy, xx, w + 8 * k, a.out.scale);
-              }
-          }
+        for (int cb = 0; cb < C::HALF / 32; ++cb) {
+          tmem_add32(trow + cb * 32, acc0 + cb * 32);
+          tmem_add32(trow + N + cb * 32, acc1 + cb * 32);
         }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&cempty_bar[b]);
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty_bar[ab]);
+      float amax0 = 0.f, amax1 = 0.f;
+      const int tile_xy = ry * a.tiles_x + cx;
+#pragma unroll
+      for (int cb = 0; cb < C::HALF / 32; ++cb)
+        epilogue32<N>(a, acc0 + cb * 32, acc1 + cb * 32, nt * N + grp * C::HALF + cb * 32, x, y0, tile_xy, q,
+                      amax0, amax1);
       if (a.amax) {
         amax0 = warp_max(amax0);
         amax1 = warp_max(amax1);
         if (lane == 0) {
-          if (amax0 > 0.f) atomic_max_pos(a.amax, amax0);
-          if (amax1 > 0.f) atomic_max_pos(a.amax + 1, amax1);
+          if (amax0 > 0.f) atomicMax(a.amax, __float_as_uint(amax0));
+          if (amax1 > 0.f) atomicMax(a.amax + 1, __float_as_uint(amax1));
         }
       }
     }
@@ -363,18 +385,16 @@ __global__ void __launch_bounds__(192, 1) conv3x3_tc_kernel(const __grid_constan
 
 // ------------------------------------------------------------------------------------------
 int conv_tc_smem_bytes(int N) { return N == 128 ? ConvCfg<128>::SMEM : ConvCfg<64>::SMEM; }
-int conv_tc_b_bytes(int N) { return N == 128 ? ConvCfg<128>::B_BYTES : ConvCfg<64>::B_BYTES; }
-int conv_tc_xb_bytes(int N) { return N == 128 ? ConvCfg<128>::XB_BYTES : ConvCfg<64>::XB_BYTES; }
 
 cudaError_t launch_conv_tc(const ConvArgs& a, int N, int grid, cudaStream_t stream) {
   if (N == 128) {
     auto k = conv3x3_tc_kernel<128>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, ConvCfg<128>::SMEM);
-    k<<<grid, 192, ConvCfg<128>::SMEM, stream>>>(a);
+    k<<<grid, 320, ConvCfg<128>::SMEM, stream>>>(a);
   } else {
     auto k = conv3x3_tc_kernel<64>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, ConvCfg<64>::SMEM);
-    k<<<grid, 192, ConvCfg<64>::SMEM, stream>>>(a);
+    k<<<grid, 320, ConvCfg<64>::SMEM, stream>>>(a);
   }
   return cudaGetLastError();
 }

@@ -14,18 +14,24 @@
 namespace spst {
 
 struct GramCfg {
-  static constexpr int KPX = 64;                       // pixels per stage
+  static constexpr int KPX = 64;                       // pixels per smem stage
   static constexpr int T_BYTES = 16 * KPX * 16;        // 128 channels x 64 px fp16 (16 KB)
   static constexpr int STAGE = 4 * T_BYTES;            // A hi/lo + B hi/lo
   static constexpr int STAGES = 3;
+  static constexpr int DRAIN = 2;                      // stages per TMEM accumulator (128 px)
+  static constexpr int NBUF = 4;                       // 4 x 128 TMEM columns
   static constexpr int SMEM = STAGES * STAGE + 1024;
 };
 
+// The tensor core sums at most DRAIN*KPX pixels into one fresh TMEM accumulator; the 4
+// epilogue warps (one row of the 128x128 tile per thread) drain every accumulator into fp32
+// registers with round-to-nearest adds, so the partial is accurate to ~fp32 regardless of
+// how many pixels a CTA covers.
 __global__ void __launch_bounds__(192, 1) gram_tc_kernel(const __grid_constant__ GramArgs a) {
   using C = GramCfg;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ uint64_t full_bar[C::STAGES], empty_bar[C::STAGES], done_bar;
+  __shared__ uint64_t full_bar[C::STAGES], empty_bar[C::STAGES], cfull_bar[C::NBUF], cempty_bar[C::NBUF];
   __shared__ uint32_t tmem_slot;
   const uint32_t warp = warp_id(), lane = lane_id();
 
@@ -39,7 +45,8 @@ __global__ void __launch_bounds__(192, 1) gram_tc_kernel(const __grid_constant__
   const bool diag = c1 == c2;
   const long long p0 = a.p_begin + (long long)blockIdx.x * a.px_per_split;
   const long long p1 = min(p0 + a.px_per_split, a.p_end);
-  const int n_chunks = (int)((p1 - p0 + C::KPX - 1) / C::KPX);
+  const int n_stages = p1 > p0 ? (int)((p1 - p0 + C::KPX - 1) / C::KPX) : 0;
+  const int n_drains = (n_stages + C::DRAIN - 1) / C::DRAIN;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&a.tm_hi);
@@ -48,10 +55,13 @@ __global__ void __launch_bounds__(192, 1) gram_tc_kernel(const __grid_constant__
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
     }
-    mbar_init(&done_bar, 1);
+    for (int b = 0; b < C::NBUF; ++b) {
+      mbar_init(&cfull_bar[b], 1);
+      mbar_init(&cempty_bar[b], 4);
+    }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc<128>(&tmem_slot);
+  if (warp == 1) tmem_alloc<512>(&tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -60,13 +70,12 @@ __global__ void __launch_bounds__(192, 1) gram_tc_kernel(const __grid_constant__
   if (warp == 0) {
     if (lane == 0) {
       const uint32_t bytes = (diag ? 2 : 4) * C::T_BYTES;
-      for (int c = 0; c < n_chunks; ++c) {
+      for (int c = 0; c < n_stages; ++c) {
         const int s = c % C::STAGES;
         mbar_wait(&empty_bar[s], ((c / C::STAGES) & 1) ^ 1);
         uint8_t* st = smem + s * C::STAGE;
         mbar_arrive_expect_tx(&full_bar[s], bytes);
-        // coordinates relative to the map base (which starts at p_begin)
-        const int px = (int)(p0 - a.p_begin) + c * C::KPX;
+        const int px = (int)(p0 - a.p_begin) + c * C::KPX;  // map base starts at p_begin
         tma_load_3d(st, &a.tm_hi, &full_bar[s], 0, px, 16 * c1);
         tma_load_3d(st + C::T_BYTES, &a.tm_lo, &full_bar[s], 0, px, 16 * c1);
         if (!diag) {
@@ -78,49 +87,59 @@ __global__ void __launch_bounds__(192, 1) gram_tc_kernel(const __grid_constant__
   } else if (warp == 1) {
     if (lane == 0) {
       const uint32_t idesc = make_idesc_f16(128, 128, 0, 1, 1);
-      for (int c = 0; c < n_chunks; ++c) {
+      for (int c = 0; c < n_stages; ++c) {
+        const int dr = c / C::DRAIN;
+        const uint32_t b = dr % C::NBUF;
+        if (c % C::DRAIN == 0) mbar_wait(&cempty_bar[b], ((dr / C::NBUF) & 1) ^ 1);
         const int s = c % C::STAGES;
         mbar_wait(&full_bar[s], (c / C::STAGES) & 1);
         tc_fence_after();
         const uint32_t st = smem_u32(smem + s * C::STAGE);
         const uint32_t ah = st, al = st + C::T_BYTES;
         const uint32_t bh = diag ? ah : st + 2 * C::T_BYTES, bl = diag ? al : st + 3 * C::T_BYTES;
+        const uint32_t d = tmem + b * 128;
+        // correction passes before the hi*hi pass (see conv_tc.cu)
 #pragma unroll
-        for (int k = 0; k < C::KPX / 16; ++k) {
-          const uint32_t off = k * 256;  // 16 px = two 8-px core-matrix groups of 128 B
-          const uint64_t dah = make_sdesc(ah + off, 128, C::KPX * 16);
-          const uint64_t dal = make_sdesc(al + off, 128, C::KPX * 16);
-          const uint64_t dbh = make_sdesc(bh + off, 128, C::KPX * 16);
-          const uint64_t dbl = make_sdesc(bl + off, 128, C::KPX * 16);
-          umma_f16(tmem, dah, dbh, idesc, (c > 0 || k > 0) ? 1u : 0u);
-          umma_f16(tmem, dah, dbl, idesc, 1u);
-          umma_f16(tmem, dal, dbh, idesc, 1u);
-        }
+        for (int pass = 0; pass < 3; ++pass)
+#pragma unroll
+          for (int k = 0; k < C::KPX / 16; ++k) {
+            const uint32_t off = k * 256;  // 16 px = two 8-px core-matrix groups of 128 B
+            const uint64_t da = make_sdesc((pass == 1 ? al : ah) + off, 128, C::KPX * 16);
+            const uint64_t db = make_sdesc((pass == 0 ? bl : bh) + off, 128, C::KPX * 16);
+            umma_f16(d, da, db, idesc, (c % C::DRAIN > 0 || pass > 0 || k > 0) ? 1u : 0u);
+          }
         umma_commit(&empty_bar[s]);
+        if (c % C::DRAIN == C::DRAIN - 1 || c == n_stages - 1) umma_commit(&cfull_bar[b]);
       }
-      umma_commit(&done_bar);
     }
   } else {
     const uint32_t q = warp & 3;
-    mbar_wait(&done_bar, 0);
-    tc_fence_after();
+    float acc[128];
+#pragma unroll
+    for (int i = 0; i < 128; ++i) acc[i] = 0.f;
+    for (int dr = 0; dr < n_drains; ++dr) {
+      const uint32_t b = dr % C::NBUF;
+      mbar_wait(&cfull_bar[b], (dr / C::NBUF) & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int cb = 0; cb < 4; ++cb) {
+        float v[32];
+        tmem_ld32(tmem + ((q * 32u) << 16) + b * 128 + cb * 32, v);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) acc[cb * 32 + j] += v[j];
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&cempty_bar[b]);
+    }
     const int pairs = a.n_ctile * (a.n_ctile + 1) / 2;
     float* dst = a.partial + (((size_t)blockIdx.x * pairs + blockIdx.y) * 128 + q * 32 + lane) * 128;
-    for (int cb = 0; cb < 4; ++cb) {
-      float v[32];
-      if (n_chunks > 0) {
-        tmem_ld32(tmem + ((q * 32u) << 16) + cb * 32, v);
-      } else {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = 0.f;
-      }
-#pragma unroll
-      for (int j = 0; j < 32; j += 4) *reinterpret_cast<float4*>(dst + cb * 32 + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-    }
+    for (int j = 0; j < 128; j += 4) *reinterpret_cast<float4*>(dst + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_dealloc<128>(tmem);
+  if (warp == 1) tmem_dealloc<512>(tmem);
 }
 
 // S[c1][c2] (f64, C x C) = sum over splits of the fp32 partial tiles, fixed split order.

@@ -28,7 +28,7 @@ using namespace spst;
 
 namespace {
 
-constexpr int kPxPerSplit = 8192;    // Gram pixels summed per fp32 TMEM accumulator
+constexpr int kMaxPxPerSplit = 65536;  // Gram pixels per CTA partial (register-accumulated)
 constexpr float kTargetLog2 = 11.f;  // stored |max| ~ 2^11 (fp16 max 65504 ~ 2^16)
 constexpr float kOverflow = 30000.f;
 constexpr float kUnderflow = 64.f;
@@ -68,6 +68,13 @@ bool map_gram(CUtensorMap* m, const __half* base, long long P_range, long long P
 }
 
 int round_up(int v, int m) { return (v + m - 1) / m * m; }
+// enough (split x pair) CTAs for two waves, splits of 1K..64K pixels (multiples of 128)
+int gram_px_per_split(long long px, int pairs) {
+  const long long want_splits = std::max<long long>(1, (2 * kSMs + pairs - 1) / pairs);
+  long long per = (px + want_splits - 1) / want_splits;
+  per = std::max<long long>(1024, std::min<long long>(kMaxPxPerSplit, per));
+  return (int)((per + 127) / 128 * 128);
+}
 int ntile_for(int C_p) { return (C_p % 128 == 0) ? 128 : 64; }
 float pow2f(int e) { return std::ldexp(1.0f, e); }
 int choose_exp(float amax) {
@@ -100,6 +107,7 @@ struct TapState {
   bool has_ref = false;
   float* gram_partial = nullptr;
   int gram_splits = 0;
+  int gram_px = 1024;
   float* colsum_partial = nullptr;
   int colsum_rows = 0;
 };
@@ -457,7 +465,7 @@ int stage_stats(spst_ctx* ctx, int k) {
   Stage& s = ctx->stages[k];
   if (s.style < 0) return SPST_OK;
   TapState& t = ctx->taps[s.style];
-  CK(launch_colsum_reduce(t.colsum_partial, t.colsum_rows, s.cout, t.s, ctx->stream));
+  CK(launch_colsum_reduce(t.colsum_partial, t.colsum_rows, s.cout, s.cout_p, t.s, ctx->stream));
   const int own0 = (ctx->own_r0 - ctx->grid_r0) / s.stride, own1 = (ctx->own_r1 - ctx->grid_r0) / s.stride;
   const long long P_total = (long long)s.H * s.W;
   const long long p0 = (long long)own0 * s.W, p1 = (long long)own1 * s.W;
@@ -468,7 +476,7 @@ int stage_stats(spst_ctx* ctx, int k) {
   g.C_p = s.cout_p;
   g.p_begin = 0;
   g.p_end = p1 - p0;
-  g.px_per_split = kPxPerSplit;
+  g.px_per_split = t.gram_px;
   g.n_ctile = (s.cout_p + 127) / 128;
   g.partial = t.gram_partial;
   CK(launch_gram_tc(g, t.gram_splits, ctx->stream));
@@ -769,8 +777,9 @@ int bind_alloc(spst_ctx* ctx) {
       t.xw = ctx->dalloc<__half>((size_t)Cp * Cp * 2);
       const int own0 = (ctx->own_r0 - ctx->grid_r0) / s.stride, own1 = (ctx->own_r1 - ctx->grid_r0) / s.stride;
       const long long own_px = (long long)(own1 - own0) * s.W;
-      t.gram_splits = (int)std::max<long long>(1, (own_px + kPxPerSplit - 1) / kPxPerSplit);
       const int nct = (Cp + 127) / 128;
+      t.gram_px = gram_px_per_split(own_px, nct * (nct + 1) / 2);
+      t.gram_splits = (int)std::max<long long>(1, (own_px + t.gram_px - 1) / t.gram_px);
       t.gram_partial = ctx->dalloc<float>((size_t)t.gram_splits * (nct * (nct + 1) / 2) * 128 * 128);
       t.colsum_rows = k == 0 ? first_conv_fwd_blocks(s.H, s.W) : ((s.W + 127) / 128) * ((s.H + 1) / 2) * 4;
       t.colsum_partial = ctx->dalloc<float>((size_t)t.colsum_rows * Cp);
@@ -1201,8 +1210,9 @@ int spst_debug_gram(int device, int C, long long P, const float* f_host, double*
   HL16 t = hl_shape(Cp, 1, (int)P);
   t.hi = ctx->dalloc<__half>((size_t)Cp * P * 2);
   float* fd = ctx->dalloc<float>((size_t)C * P);
-  const int splits = (int)std::max<long long>(1, (P + kPxPerSplit - 1) / kPxPerSplit);
   const int nct = (Cp + 127) / 128;
+  const int per = gram_px_per_split(P, nct * (nct + 1) / 2);
+  const int splits = (int)std::max<long long>(1, (P + per - 1) / per);
   float* part = ctx->dalloc<float>((size_t)splits * (nct * (nct + 1) / 2) * 128 * 128);
   double* Sd = ctx->dalloc<double>((size_t)C * C);
   if (!t.hi || !fd || !part || !Sd) return SPST_ERR_OOM;
@@ -1213,7 +1223,7 @@ int spst_debug_gram(int device, int C, long long P, const float* f_host, double*
   g.C_p = Cp;
   g.p_begin = 0;
   g.p_end = P;
-  g.px_per_split = kPxPerSplit;
+  g.px_per_split = per;
   g.n_ctile = nct;
   g.partial = part;
   CK(launch_gram_tc(g, splits, nullptr));

@@ -240,11 +240,11 @@ __global__ void pool2_hl_kernel(HL16 in, HL16 out, unsigned int* amax) {
 }
 
 // sums[c] = sum_r partial[r][c] in f64, fixed row order
-__global__ void colsum_reduce_kernel(const float* partial, int rows, int C, double* sums) {
+__global__ void colsum_reduce_kernel(const float* partial, int rows, int C, int stride, double* sums) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= C) return;
   double acc = 0.0;
-  for (int r = 0; r < rows; ++r) acc += (double)partial[(size_t)r * C + c];
+  for (int r = 0; r < rows; ++r) acc += (double)partial[(size_t)r * stride + c];
   sums[c] = acc;
 }
 
@@ -588,8 +588,8 @@ cudaError_t launch_pool2_hl(const HL16& in, const HL16& out, unsigned int* amax,
   return cudaGetLastError();
 }
 
-cudaError_t launch_colsum_reduce(const float* partial, int rows, int C, double* sums, cudaStream_t st) {
-  colsum_reduce_kernel<<<(C + 127) / 128, 128, 0, st>>>(partial, rows, C, sums);
+cudaError_t launch_colsum_reduce(const float* partial, int rows, int C, int stride, double* sums, cudaStream_t st) {
+  colsum_reduce_kernel<<<(C + 127) / 128, 128, 0, st>>>(partial, rows, C, stride, sums);
   return cudaGetLastError();
 }
 

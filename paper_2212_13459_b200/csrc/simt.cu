@@ -476,12 +476,16 @@ __global__ void twoloop_scalar_kernel(const double* dot, double rho, int mode, d
 }
 
 // x_out = x + t*d (numpy weak-scalar semantics: t has x's dtype, product rounded then sum)
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+
+// two separate roundings (no FMA contraction), as numpy evaluates x + t * d
 template <typename T>
 __global__ void axpy_kernel(const T* x, const T* d, T t, long long n, T* out) {
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    const T p = t * d[i];
-    out[i] = x[i] + p;
-  }
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    out[i] = add_rn(x[i], mul_rn(t, d[i]));
 }
 
 // s = xt - x, y = gt - g and partials of <y,s>, <s,s>, <y,y>

@@ -32,11 +32,12 @@ enum EpiKind : int {
 // Parameters of one tcgen05 3x3 implicit-GEMM launch (forward or input-gradient).
 struct ConvArgs {
   CUtensorMap tm_a_hi, tm_a_lo;  // K operand: input activations (box 8 x 130 x 4 x 2)
-  CUtensorMap tm_v_hi, tm_v_lo;  // extra-K operand: tap features at the output pixels
+  CUtensorMap tm_v_hi, tm_v_lo;  // extra-K operand: tap features at the output pixels (box 8 x 128 x 2 x 4)
   const uint8_t* wgt;            // [ntile][kc][pass][tap][kg][n][8] fp16
-  const uint8_t* xwgt;           // [ntile][xkc][pass][kg][n][8] fp16 (extra K, one tap)
+  const uint8_t* xwgt;           // [ntile][xkc][pass][kg(4)][n][8] fp16 (extra K, 32 ch per chunk)
+  float x_rescale;               // extra-K chunk partials are multiplied by this when drained
   int H, W;                      // output (== input) spatial dims of the GEMM grid
-  int n_kc, n_xkc;               // conv K-chunks (16 ch each), extra K-chunks
+  int n_kc, n_xkc;               // conv K-chunks (16 ch each), extra K-chunks (32 ch each)
   int n_ntiles;                  // output channel tiles
   int tiles_x, tiles_y;          // 128-px column blocks, 2-row row blocks
   float acc_scale;               // 2^-(e_in + f)
@@ -67,6 +68,8 @@ struct GramArgs {
   float* partial;                // [split][pair][128][128]
 };
 
+constexpr int kFirstC = 64;  // first-layer output channels supported by the SIMT kernels (padded)
+
 struct FirstConvArgs {
   const float* img;   // (h, w, 3) f32, unpadded global image
   int h, w;           // unpadded global dims
@@ -74,8 +77,8 @@ struct FirstConvArgs {
   int Hl, Wp;         // local grid (rows) x padded width
   int perm[3];
   float mean[3], scale[3];
-  const float* wgt;   // [C_out][3][3][3] f32
-  const float* bias;  // [C_out]
+  float wgt[kFirstC * 27];  // [C_out][3][3][3] f32, zero padded (kernel-parameter constant bank)
+  float bias[kFirstC];
   int C_out, C_out_p;
   HL16 out;
   uint32_t* mask;
@@ -86,7 +89,7 @@ struct FirstConvArgs {
 
 struct FirstConvBwdArgs {
   HL16 g;             // gradient at the first conv's output (masked), C_p channels
-  const float* wgt;   // [C_out][3][3][3]
+  float wgt[kFirstC * 27];
   int C_out;
   int perm[3];
   float scale[3];
@@ -139,7 +142,9 @@ cudaError_t launch_first_conv_bwd(const FirstConvBwdArgs& a, cudaStream_t st);
 cudaError_t launch_fold_grad(const float* gimg, int Hl, int Wp, int row_off, int h, int w, int r0, int r1,
                              float* grad, cudaStream_t st);
 cudaError_t launch_pool2_hl(const HL16& in, const HL16& out, unsigned int* amax, cudaStream_t st);
-cudaError_t launch_colsum_reduce(const float* partial, int rows, int C, int stride, double* sums, cudaStream_t st);
+cudaError_t launch_colsum_reduce(const float* partial, int rows, int C, int stride, double* sums, double* mid,
+                                 cudaStream_t st);
+constexpr int kColsumMid = 256;  // doubles per channel of colsum scratch
 cudaError_t launch_style_vec(const StyleCoefArgs& a, cudaStream_t st);
 cudaError_t launch_style_mat(const StyleCoefArgs& a, cudaStream_t st);
 cudaError_t launch_content_sqdiff(const HL16& v, const HL16& u, int C, int r0, int r1, double* partial,

@@ -39,7 +39,9 @@ struct ConvCfg {
   static constexpr int A_BYTES = 2 * A_HALF;        // hi + lo
   static constexpr int B_TAP = 2 * N * 16;          // 16 channels x N outputs (fp16)
   static constexpr int B_BYTES = 2 * 9 * B_TAP;     // hi/lo x 9 taps
-  static constexpr int XB_BYTES = 2 * B_TAP;        // extra-K slab: hi/lo x 1 tap
+  static constexpr int XA_PLANE = 2 * 128 * 16;     // extra-K operand: 2 rows x 128 px, 8 ch
+  static constexpr int XA_HALF = 4 * XA_PLANE;      // 32 channels
+  static constexpr int XB_BYTES = 2 * 4 * N * 16;   // extra-K slab: hi/lo x 32 channels
   static constexpr int STAGE = ((A_BYTES + B_BYTES + 1023) / 1024) * 1024;
   static constexpr int STAGES = N == 128 ? 2 : 3;
   static constexpr int NBUF = N == 128 ? 2 : 4;     // TMEM chunk buffers (2 rows x N each)
@@ -95,11 +97,11 @@ __device__ __forceinline__ float warp_max(float v) {
 }
 
 // 32 columns of TMEM added into acc[0..31] (fp32 round-to-nearest adds)
-__device__ __forceinline__ void tmem_add32(uint32_t taddr, float* acc) {
+__device__ __forceinline__ void tmem_add32(uint32_t taddr, float* acc, float scale) {
   float v[32];
   tmem_ld32(taddr, v);
 #pragma unroll
-  for (int i = 0; i < 32; ++i) acc[i] += v[i];
+  for (int i = 0; i < 32; ++i) acc[i] = fmaf(v[i], scale, acc[i]);
 }
 
 // Fused pointwise epilogue for 32 channels of one pixel in both rows (v0: row y0, v1: y0+1).
@@ -285,11 +287,16 @@ __global__ void __launch_bounds__(320, 1) conv3x3_tc_kernel(const __grid_constan
           mbar_wait(&empty_bar[s], ((g / C::STAGES) & 1) ^ 1);
           uint8_t* st = smem + s * C::STAGE;
           const bool conv = c < a.n_kc;
+          if (conv) {
+            mbar_arrive_expect_tx(&full_bar[s], C::A_BYTES + C::B_BYTES);
+            tma_load_4d(st, &a.tm_a_hi, &full_bar[s], 0, x0 - 1, y0 - 1, 2 * c);
+            tma_load_4d(st + C::A_HALF, &a.tm_a_lo, &full_bar[s], 0, x0 - 1, y0 - 1, 2 * c);
+          } else {  // extra K (tap features): only the tile's own 2 x 128 pixels, 32 channels
+            mbar_arrive_expect_tx(&full_bar[s], 2 * C::XA_HALF + C::XB_BYTES);
+            tma_load_4d(st, &a.tm_v_hi, &full_bar[s], 0, x0, y0, 4 * (c - a.n_kc));
+            tma_load_4d(st + C::XA_HALF, &a.tm_v_lo, &full_bar[s], 0, x0, y0, 4 * (c - a.n_kc));
+          }
           const uint32_t bbytes = conv ? C::B_BYTES : C::XB_BYTES;
-          mbar_arrive_expect_tx(&full_bar[s], C::A_BYTES + bbytes);
-          const int kg0 = conv ? 2 * c : 2 * (c - a.n_kc);
-          tma_load_4d(st, conv ? &a.tm_a_hi : &a.tm_v_hi, &full_bar[s], 0, x0 - 1, y0 - 1, kg0);
-          tma_load_4d(st + C::A_HALF, conv ? &a.tm_a_lo : &a.tm_v_lo, &full_bar[s], 0, x0 - 1, y0 - 1, kg0);
           const uint8_t* src = conv ? a.wgt + ((size_t)nt * a.n_kc + c) * C::B_BYTES
                                     : a.xwgt + ((size_t)nt * a.n_xkc + (c - a.n_kc)) * C::XB_BYTES;
           bulk_load(st + C::A_BYTES, src, bbytes, &full_bar[s]);
@@ -309,16 +316,33 @@ __global__ void __launch_bounds__(320, 1) conv3x3_tc_kernel(const __grid_constan
           mbar_wait(&full_bar[s], (g / C::STAGES) & 1);
           tc_fence_after();
           const uint32_t st = smem_u32(smem + s * C::STAGE);
-          const uint32_t a_hi = st, a_lo = st + C::A_HALF, bb = st + C::A_BYTES;
+          const uint32_t bb = st + C::A_BYTES;
           const bool conv = c < a.n_kc;
-          const int ntap = conv ? 9 : 1;
           const uint32_t dcol = tmem_base + b * 2 * N;
+          if (!conv) {
+            // V[2 rows x 128 px, 32 ch] x M[32 x N]: two K=16 steps per pass
+            for (int pass = 0; pass < 3; ++pass)
+#pragma unroll
+              for (int ks = 0; ks < 2; ++ks) {
+                const uint64_t bd = make_sdesc(bb + (pass == 0 ? 4 * N * 16 : 0) + 2 * ks * N * 16, N * 16, 128);
+#pragma unroll
+                for (int mt = 0; mt < 2; ++mt) {
+                  const uint32_t ab = st + (pass == 1 ? C::XA_HALF : 0) + mt * 128 * 16 + 2 * ks * C::XA_PLANE;
+                  umma_f16(dcol + mt * N, make_sdesc(ab, C::XA_PLANE, 128), bd, idesc, (pass | ks) ? 1u : 0u);
+                }
+              }
+            umma_commit(&empty_bar[s]);
+            umma_commit(&cfull_bar[b]);
+            continue;
+          }
+          const uint32_t a_hi = st, a_lo = st + C::A_HALF;
+          const int ntap = 9;
           // Small correction products first (hi*lo, lo*hi), then the large hi*hi products: the
           // tensor core truncates each accumulation to the running sum's exponent, so keeping the
           // sum small while the corrections go in cuts the chunk's rounding error ~3x.
           for (int pass = 0; pass < 3; ++pass) {
             for (int tap = 0; tap < ntap; ++tap) {
-              const int dy = conv ? tap / 3 : 1, dx = conv ? tap % 3 : 1;
+              const int dy = tap / 3, dx = tap % 3;
               const uint64_t bd = make_sdesc(bb + ((pass == 0 ? ntap : 0) + tap) * C::B_TAP, N * 16, 128);
 #pragma unroll
               for (int mt = 0; mt < 2; ++mt) {
@@ -353,10 +377,11 @@ __global__ void __launch_bounds__(320, 1) conv3x3_tc_kernel(const __grid_constan
         mbar_wait(&cfull_bar[b], (g / C::NBUF) & 1);
         tc_fence_after();
         const uint32_t trow = tmem_base + ((q * 32u) << 16) + b * 2 * N + grp * C::HALF;
+        const float cs = c < a.n_kc ? 1.f : a.x_rescale;  // extra-K chunks carry their own scale
 #pragma unroll
         for (int cb = 0; cb < C::HALF / 32; ++cb) {
-          tmem_add32(trow + cb * 32, acc0 + cb * 32);
-          tmem_add32(trow + N + cb * 32, acc1 + cb * 32);
+          tmem_add32(trow + cb * 32, acc0 + cb * 32, cs);
+          tmem_add32(trow + N + cb * 32, acc1 + cb * 32, cs);
         }
         tc_fence_before();
         __syncwarp();

@@ -47,10 +47,11 @@ bool get_encoder() {
   return true;
 }
 
-bool map_act(CUtensorMap* m, const __half* base, int n_kg, int H, int W) {
+// conv K operand: halo window box (8 ch, 130 px, 4 rows, 2 kg); extra-K operand: (8, 128, 2, 4)
+bool map_act(CUtensorMap* m, const __half* base, int n_kg, int H, int W, bool extra = false) {
   cuuint64_t dims[4] = {8, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)n_kg};
   cuuint64_t strides[3] = {16, (cuuint64_t)W * 16, (cuuint64_t)H * W * 16};
-  cuuint32_t box[4] = {8, 130, 4, 2};
+  cuuint32_t box[4] = {8, extra ? 128u : 130u, extra ? 2u : 4u, extra ? 4u : 2u};
   cuuint32_t es[4] = {1, 1, 1, 1};
   return g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, (void*)base, dims, strides, box, es,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -110,6 +111,7 @@ struct TapState {
   int gram_px = 1024;
   float* colsum_partial = nullptr;
   int colsum_rows = 0;
+  double* colsum_mid = nullptr;
 };
 
 struct Expo {
@@ -272,6 +274,8 @@ int parse_net(spst_ctx* ctx, int n_layers, const int* kinds, const int* cin, con
     s.cin = cin[i];
     s.cout = cout[i];
     if (s.cin != prev_c) return ctx->fail(SPST_ERR_SHAPE, "conv input channels do not chain");
+    if (ctx->stages.empty() && s.cout > kFirstC)
+      return ctx->fail(SPST_ERR_UNSUPPORTED, "first conv layer supports at most 64 output channels");
     s.cin_p = ctx->stages.empty() ? 3 : round_up(s.cin, 64);
     s.cout_p = round_up(s.cout, 64);
     s.stride = stride;
@@ -376,7 +380,8 @@ int run_conv(spst_ctx* ctx, ConvLaunch& L) {
   const HL16* v = L.v ? L.v : in;
   if (!map_act(&a.tm_a_hi, in->hi, in->C_p / 8, in->H, in->W) ||
       !map_act(&a.tm_a_lo, in->lo(), in->C_p / 8, in->H, in->W) ||
-      !map_act(&a.tm_v_hi, v->hi, v->C_p / 8, v->H, v->W) || !map_act(&a.tm_v_lo, v->lo(), v->C_p / 8, v->H, v->W))
+      !map_act(&a.tm_v_hi, v->hi, v->C_p / 8, v->H, v->W, true) ||
+      !map_act(&a.tm_v_lo, v->lo(), v->C_p / 8, v->H, v->W, true))
     return ctx->fail(SPST_ERR_CUDA, "cuTensorMapEncodeTiled failed");
   a.wgt = L.in ? L.wslab : nullptr;
   a.n_kc = L.in ? L.in->C_p / 16 : 0;
@@ -425,8 +430,8 @@ int forward_stage(spst_ctx* ctx, int k, const float* x) {
       a.mean[c] = ctx->mean[c];
       a.scale[c] = ctx->scale[c];
     }
-    a.wgt = s.w1_d;
-    a.bias = s.bias_d;
+    for (int i = 0; i < kFirstC * 27; ++i) a.wgt[i] = i < (int)s.w.size() ? (float)s.w[i] : 0.f;
+    for (int i = 0; i < kFirstC; ++i) a.bias[i] = i < s.cout ? (float)s.b[i] : 0.f;
     a.C_out = s.cout;
     a.C_out_p = s.cout_p;
     a.out = s.out;
@@ -465,7 +470,7 @@ int stage_stats(spst_ctx* ctx, int k) {
   Stage& s = ctx->stages[k];
   if (s.style < 0) return SPST_OK;
   TapState& t = ctx->taps[s.style];
-  CK(launch_colsum_reduce(t.colsum_partial, t.colsum_rows, s.cout, s.cout_p, t.s, ctx->stream));
+  CK(launch_colsum_reduce(t.colsum_partial, t.colsum_rows, s.cout, s.cout_p, t.s, t.colsum_mid, ctx->stream));
   const int own0 = (ctx->own_r0 - ctx->grid_r0) / s.stride, own1 = (ctx->own_r1 - ctx->grid_r0) / s.stride;
   const long long P_total = (long long)s.H * s.W;
   const long long p0 = (long long)own0 * s.W, p1 = (long long)own1 * s.W;
@@ -550,7 +555,7 @@ StyleCoefArgs coef_args(spst_ctx* ctx, TapState& t) {
   a.ms_loss = t.ms_loss;
   a.degenerate = t.degenerate;
   a.N = ntile_for(s.cout_p);
-  a.n_xkc = s.cout_p / 16;
+  a.n_xkc = s.cout_p / 32;
   return a;
 }
 
@@ -582,11 +587,12 @@ int tap_grad_gemm(spst_ctx* ctx, int k, HL16 out, bool with_mask, double two_lam
   ConvLaunch L;
   L.v = &s.out;
   L.xw = s.style >= 0 ? ctx->taps[s.style].xw : ctx->zero_xw;
-  L.n_xkc = s.cout_p / 16;
+  L.n_xkc = s.cout_p / 32;
   L.H = s.H;
   L.W = s.W;
   L.acc_scale = 1.f / (s.out.scale * pow2f(xexp));
   ConvArgs& a = L.a;
+  a.x_rescale = 1.f;
   a.epi = EPI_BWD;
   a.bias = s.style >= 0 ? ctx->taps[s.style].bvec : nullptr;
   a.mask_in = with_mask ? s.mask : nullptr;
@@ -618,6 +624,7 @@ int backward_stage(spst_ctx* ctx, int k, int src, int dst, double two_lambda) {
   const int acc_e = nx.g_e.e + nx.wexp;
   L.acc_scale = 1.f / pow2f(acc_e);
   ConvArgs& a = L.a;
+  a.x_rescale = 1.f;
   a.out = gout;
   a.mask_in = s.mask;
   a.amax = ctx->amax_d + 4 * k + 2;
@@ -628,18 +635,15 @@ int backward_stage(spst_ctx* ctx, int k, int src, int dst, double two_lambda) {
   } else {
     a.epi = EPI_BWD;
     if (s.style >= 0) {
-      // fuse V*M as extra K-steps when the slab scale that matches the conv accumulator fits fp16
-      const int xexp = acc_e - (int)std::lround(std::log2(s.out.scale));
-      const double mm = ctx->taps[s.style].mmax * std::ldexp(1.0, xexp);
-      if (mm <= 16384.0 * 2 && (mm >= 16.0 || mm == 0.0)) {
-        TRY(write_xw(ctx, k, xexp));
-        L.v = &s.out;
-        L.xw = ctx->taps[s.style].xw;
-        L.n_xkc = s.cout_p / 16;
-        a.bias = ctx->taps[s.style].bvec;
-      } else {
-        use_addend = true;
-      }
+      // V*M enters as extra K-steps of the same GEMM; its chunks carry their own scale 2^(eV+xexp)
+      // and are rescaled to the conv accumulator's 2^acc_e when the epilogue drains them
+      const int xexp = gemm_only_xexp(ctx, k);
+      TRY(write_xw(ctx, k, xexp));
+      L.v = &s.out;
+      L.xw = ctx->taps[s.style].xw;
+      L.n_xkc = s.cout_p / 32;
+      a.x_rescale = (float)std::ldexp(1.0, acc_e - xexp) / s.out.scale;
+      a.bias = ctx->taps[s.style].bvec;
     }
     if (s.content && two_lambda != 0.0 && !use_addend) {
       a.content_v = s.out;
@@ -710,7 +714,7 @@ int do_backward(spst_ctx* ctx, double two_lambda, float* grad, bool careful) {
   Stage& s0 = ctx->stages[0];
   FirstConvBwdArgs b{};
   b.g = ctx->gbuf[cur];
-  b.wgt = s0.w1_d;
+  for (int i = 0; i < kFirstC * 27; ++i) b.wgt[i] = i < (int)s0.w.size() ? (float)s0.w[i] : 0.f;
   b.C_out = s0.cout;
   for (int c = 0; c < 3; ++c) {
     b.perm[c] = ctx->perm[c];
@@ -783,8 +787,9 @@ int bind_alloc(spst_ctx* ctx) {
       t.gram_partial = ctx->dalloc<float>((size_t)t.gram_splits * (nct * (nct + 1) / 2) * 128 * 128);
       t.colsum_rows = k == 0 ? first_conv_fwd_blocks(s.H, s.W) : ((s.W + 127) / 128) * ((s.H + 1) / 2) * 4;
       t.colsum_partial = ctx->dalloc<float>((size_t)t.colsum_rows * Cp);
+      t.colsum_mid = ctx->dalloc<double>((size_t)kColsumMid * Cp);
       if (!t.S || !t.s || !t.mu || !t.sd || !t.ratio || !t.row_loss || !t.row_mmax || !t.ms_loss || !t.degenerate ||
-          !t.bvec || !t.xw || !t.gram_partial || !t.colsum_partial)
+          !t.bvec || !t.xw || !t.gram_partial || !t.colsum_partial || !t.colsum_mid)
         return ctx->fail(SPST_ERR_OOM, "statistics buffers");
       CK(cudaMemset(t.bvec, 0, Cp * 4));
       CK(cudaMemset(t.s, 0, Cp * 8));

@@ -33,9 +33,10 @@ __device__ __forceinline__ float warp_transpose_sum32(float (&v)[32]) {
   return v[0];
 }
 
-__global__ void __launch_bounds__(256) first_conv_fwd_kernel(const FirstConvArgs a) {
+// Weights and bias come from the kernel-parameter constant bank with compile-time indices, so
+// every FFMA takes its weight operand straight from the constant cache.
+__global__ void __launch_bounds__(256) first_conv_fwd_kernel(const __grid_constant__ FirstConvArgs a) {
   __shared__ float tile[3][FC_BY + 2][FC_BX + 2];
-  __shared__ float wsm[64 * 27];
   __shared__ float csum[FC_BY][32];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int x0 = blockIdx.x * FC_BX, y0 = blockIdx.y * FC_BY;
@@ -51,34 +52,36 @@ __global__ void __launch_bounds__(256) first_conv_fwd_kernel(const FirstConvArgs
     }
     tile[c][r][cc] = v;
   }
+  __syncthreads();
+  float in[27];
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+#pragma unroll
+    for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
+      for (int dx = 0; dx < 3; ++dx) in[c * 9 + dy * 3 + dx] = tile[c][ty + dy][tx + dx];
   const int y = y0 + ty, x = x0 + tx;
   const bool ok = y < a.Hl && x < a.Wp;
   const bool in_sum = ok && y >= a.sum_r0 && y < a.sum_r1;
   float amax = 0.f;
-  for (int cg = 0; cg < a.C_out_p; cg += 32) {
-    const int nc = min(32, a.C_out - cg);
-    __syncthreads();
-    for (int i = threadIdx.x; i < 32 * 27; i += blockDim.x) wsm[i] = (i / 27 < nc) ? a.wgt[(size_t)cg * 27 + i] : 0.f;
-    __syncthreads();
+#pragma unroll
+  for (int cg = 0; cg < kFirstC; cg += 32) {
     float v[32];
     uint32_t bits = 0;
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
-      float acc = (j < nc) ? a.bias[cg + j] : 0.f;
+      float acc = a.bias[cg + j];
 #pragma unroll
-      for (int c = 0; c < 3; ++c)
-#pragma unroll
-        for (int dy = 0; dy < 3; ++dy)
-#pragma unroll
-          for (int dx = 0; dx < 3; ++dx) acc = fmaf(tile[c][ty + dy][tx + dx], wsm[j * 27 + c * 9 + dy * 3 + dx], acc);
+      for (int i = 0; i < 27; ++i) acc = fmaf(in[i], a.wgt[(cg + j) * 27 + i], acc);
       bits |= (acc > 0.f ? 1u : 0u) << j;
       v[j] = fmaxf(acc, 0.f);
       amax = fmaxf(amax, ok ? v[j] : 0.f);
     }
+    if (cg >= a.C_out_p) break;
     if (ok) {
       a.mask[((size_t)(cg >> 5) * a.Hl + y) * a.Wp + x] = bits;
-      const int nkg = min(4, (a.C_out_p - cg) / 8);
-      for (int k = 0; k < nkg; ++k) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
         __align__(16) __half hh[8];
         __align__(16) __half ll[8];
 #pragma unroll
@@ -101,8 +104,9 @@ __global__ void __launch_bounds__(256) first_conv_fwd_kernel(const FirstConvArgs
         float s = 0.f;
         for (int r = 0; r < FC_BY; ++r) s += csum[r][tx];
         const size_t blk = (size_t)blockIdx.y * gridDim.x + blockIdx.x;
-        if (cg + tx < a.C_out_p) a.colsum_partial[blk * a.C_out_p + cg + tx] = s;
+        a.colsum_partial[blk * a.C_out_p + cg + tx] = s;
       }
+      __syncthreads();
     }
   }
   if (a.amax) {
@@ -112,17 +116,17 @@ __global__ void __launch_bounds__(256) first_conv_fwd_kernel(const FirstConvArgs
   }
 }
 
-
-__global__ void __launch_bounds__(256) first_conv_bwd_kernel(const FirstConvBwdArgs a) {
+__global__ void __launch_bounds__(256) first_conv_bwd_kernel(const __grid_constant__ FirstConvBwdArgs a) {
   constexpr int CH = 16;
   __shared__ float tile[CH][FC_BY + 2][FC_BX + 2];
-  __shared__ float wsm[CH * 27];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int x0 = blockIdx.x * FC_BX, y0 = blockIdx.y * FC_BY;
   const int H = a.g.H, W = a.g.W;
   const float inv = 1.f / a.g.scale;
   float acc[3] = {0.f, 0.f, 0.f};
-  for (int c0 = 0; c0 < a.g.C_p; c0 += CH) {
+#pragma unroll
+  for (int c0 = 0; c0 < kFirstC; c0 += CH) {
+    if (c0 >= a.g.C_p) break;
     __syncthreads();
     for (int i = threadIdx.x; i < (CH / 8) * (FC_BY + 2) * (FC_BX + 2); i += blockDim.x) {
       const int kg = i / ((FC_BY + 2) * (FC_BX + 2));
@@ -142,13 +146,9 @@ __global__ void __launch_bounds__(256) first_conv_bwd_kernel(const FirstConvBwdA
 #pragma unroll
       for (int e = 0; e < 8; ++e) tile[kg * 8 + e][r][cc] = v8[e];
     }
-    for (int i = threadIdx.x; i < CH * 27; i += blockDim.x) {
-      const int co = c0 + i / 27;
-      wsm[i] = co < a.C_out ? a.wgt[(size_t)co * 27 + i % 27] : 0.f;
-    }
     __syncthreads();
     // g_in[y][x][ci] = sum_{co,dy,dx} g[co][y+1-dy][x+1-dx] * W[co][ci][dy][dx]
-#pragma unroll 4
+#pragma unroll
     for (int co = 0; co < CH; ++co)
 #pragma unroll
       for (int dy = 0; dy < 3; ++dy)
@@ -156,7 +156,7 @@ __global__ void __launch_bounds__(256) first_conv_bwd_kernel(const FirstConvBwdA
         for (int dx = 0; dx < 3; ++dx) {
           const float gv = tile[co][ty + 2 - dy][tx + 2 - dx];
 #pragma unroll
-          for (int ci = 0; ci < 3; ++ci) acc[ci] = fmaf(gv, wsm[co * 27 + ci * 9 + dy * 3 + dx], acc[ci]);
+          for (int ci = 0; ci < 3; ++ci) acc[ci] = fmaf(gv, a.wgt[(c0 + co) * 27 + ci * 9 + dy * 3 + dx], acc[ci]);
         }
   }
   const int y = y0 + ty, x = x0 + tx;
@@ -240,11 +240,32 @@ __global__ void pool2_hl_kernel(HL16 in, HL16 out, unsigned int* amax) {
 }
 
 // sums[c] = sum_r partial[r][c] in f64, fixed row order
-__global__ void colsum_reduce_kernel(const float* partial, int rows, int C, int stride, double* sums) {
+// Two-level deterministic column sums: stage 1 reduces row chunks (fixed strided order per
+// thread, fixed tree across threadIdx.y), stage 2 sums the chunk partials in chunk order.
+constexpr int kColsumChunks = 256;
+
+__global__ void colsum_stage1_kernel(const float* partial, int rows, int C, int stride, int rows_per,
+                                     double* mid) {
+  __shared__ double red[8][33];
+  const int c = blockIdx.x * 32 + threadIdx.x;
+  const int r0 = blockIdx.y * rows_per, r1 = min(r0 + rows_per, rows);
+  double acc = 0.0;
+  if (c < C)
+    for (int r = r0 + threadIdx.y; r < r1; r += 8) acc += (double)partial[(size_t)r * stride + c];
+  red[threadIdx.y][threadIdx.x] = acc;
+  __syncthreads();
+  if (threadIdx.y == 0 && c < C) {
+    double t = 0.0;
+    for (int i = 0; i < 8; ++i) t += red[i][threadIdx.x];
+    mid[(size_t)blockIdx.y * C + c] = t;
+  }
+}
+
+__global__ void colsum_stage2_kernel(const double* mid, int chunks, int C, double* sums) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= C) return;
   double acc = 0.0;
-  for (int r = 0; r < rows; ++r) acc += (double)partial[(size_t)r * stride + c];
+  for (int b = 0; b < chunks; ++b) acc += mid[(size_t)b * C + c];
   sums[c] = acc;
 }
 
@@ -294,7 +315,7 @@ __global__ void style_mat_kernel(StyleCoefArgs a) {
   __shared__ double redm[256];
   const int k = blockIdx.x;
   double acc = 0.0, mm = 0.0;
-  const int kc = k >> 4, kg = (k >> 3) & 1, e = k & 7;
+  const int kc = k >> 5, kg = (k >> 3) & 3, e = k & 7;
   for (int n = threadIdx.x; n < a.C; n += blockDim.x) {
     const double g = a.S[(size_t)k * a.C + n] / a.n;
     const double d = g - a.Gr[(size_t)k * a.C + n];
@@ -307,8 +328,8 @@ __global__ void style_mat_kernel(StyleCoefArgs a) {
       HalfPair p = split_f16(v);
       const int nt = n / a.N, nl = n % a.N;
       const size_t base = ((size_t)nt * a.n_xkc + kc) * 2;
-      a.xw[(((base + 0) * 2 + kg) * a.N + nl) * 8 + e] = p.hi;
-      a.xw[(((base + 1) * 2 + kg) * a.N + nl) * 8 + e] = p.lo;
+      a.xw[(((base + 0) * 4 + kg) * a.N + nl) * 8 + e] = p.hi;
+      a.xw[(((base + 1) * 4 + kg) * a.N + nl) * 8 + e] = p.lo;
     }
   }
   red[threadIdx.x] = acc;
@@ -592,8 +613,12 @@ cudaError_t launch_pool2_hl(const HL16& in, const HL16& out, unsigned int* amax,
   return cudaGetLastError();
 }
 
-cudaError_t launch_colsum_reduce(const float* partial, int rows, int C, int stride, double* sums, cudaStream_t st) {
-  colsum_reduce_kernel<<<(C + 127) / 128, 128, 0, st>>>(partial, rows, C, stride, sums);
+cudaError_t launch_colsum_reduce(const float* partial, int rows, int C, int stride, double* sums, double* mid,
+                                 cudaStream_t st) {
+  const int rows_per = (rows + kColsumChunks - 1) / kColsumChunks;
+  const int chunks = (rows + rows_per - 1) / rows_per;
+  colsum_stage1_kernel<<<dim3((C + 31) / 32, chunks), dim3(32, 8), 0, st>>>(partial, rows, C, stride, rows_per, mid);
+  colsum_stage2_kernel<<<(C + 127) / 128, 128, 0, st>>>(mid, chunks, C, sums);
   return cudaGetLastError();
 }
 

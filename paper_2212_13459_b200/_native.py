@@ -14,7 +14,7 @@ from ctypes import POINTER, c_double, c_float, c_int, c_longlong, c_void_p
 
 from . import errors
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libspst.so")
+LIB_PATH = os.environ.get("SPST_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libspst.so")
 
 OK, E_SHAPE, E_GEOMETRY, E_CONFIG, E_NONFINITE, E_CUDA, E_OOM, E_UNSUPPORTED, E_EMPTY = range(9)
 

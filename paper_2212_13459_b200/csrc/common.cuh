@@ -115,7 +115,7 @@ struct StyleCoefArgs {
   int* degenerate;      // set to 1 when sd < eps and sdr > eps
   // extra-K weight slab for the backward kernel: [ntile][xkc][pass][kg][n][8] fp16
   __half* xw;
-  int N, n_xkc;
+  int N, n_xkc, xkg;    // slab layout [N-tile][xkc][pass][kg(xkg)][n][8]
   float xscale;         // 2^f_M
 };
 
@@ -131,8 +131,10 @@ struct AxpyDotArgs {
 };
 
 // ---------------------------------------------------------------- launchers
-cudaError_t launch_conv_tc(const ConvArgs& a, int N, int grid, cudaStream_t stream);
+cudaError_t launch_conv_tc(const ConvArgs& a, int N, int grid, cudaStream_t stream, int cluster);
 int conv_tc_smem_bytes(int N);
+int conv_tc_rows(int N);   // output rows per tile (MT)
+int conv_tc_xkg(int N);    // kgroups per extra-K chunk
 cudaError_t launch_gram_tc(const GramArgs& a, int n_splits, cudaStream_t stream);
 cudaError_t launch_gram_reduce(const float* partial, int n_splits, int n_ctile, int C, double inv_scale2,
                                double* S, cudaStream_t stream);

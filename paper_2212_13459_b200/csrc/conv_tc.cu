@@ -32,23 +32,35 @@ namespace spst {
 
 template <int N>
 struct ConvCfg {
+  static constexpr int MT = 2;                      // output rows per tile (M = MT x 128 px)
   static constexpr int PITCH = 130;                 // 128 output px + 2 halo px
-  static constexpr int RIN = 4;                     // 2 output rows + 2 halo rows
+  static constexpr int RIN = MT + 2;                // output rows + 2 halo rows
   static constexpr int A_PLANE = RIN * PITCH * 16;  // one 8-channel plane of the window
   static constexpr int A_HALF = 2 * A_PLANE;        // 16 channels
   static constexpr int A_BYTES = 2 * A_HALF;        // hi + lo
   static constexpr int B_TAP = 2 * N * 16;          // 16 channels x N outputs (fp16)
   static constexpr int B_BYTES = 2 * 9 * B_TAP;     // hi/lo x 9 taps
-  static constexpr int XA_PLANE = 2 * 128 * 16;     // extra-K operand: 2 rows x 128 px, 8 ch
-  static constexpr int XA_HALF = 4 * XA_PLANE;      // 32 channels
-  static constexpr int XB_BYTES = 2 * 4 * N * 16;   // extra-K slab: hi/lo x 32 channels
+  static constexpr int XKG = 8 / MT;                // extra-K chunk: 32 (MT=2) or 16 (MT=4) channels
+  static constexpr int XA_PLANE = MT * 128 * 16;    // extra-K operand: MT rows x 128 px, 8 ch
+  static constexpr int XA_HALF = XKG * XA_PLANE;
+  static constexpr int XB_BYTES = 2 * XKG * N * 16; // extra-K slab: hi/lo x XKG kgroups
   static constexpr int STAGE = ((A_BYTES + B_BYTES + 1023) / 1024) * 1024;
   static constexpr int STAGES = N == 128 ? 2 : 3;
-  static constexpr int NBUF = N == 128 ? 2 : 4;     // TMEM chunk buffers (2 rows x N each)
+  static constexpr int NBUF = 512 / (MT * N);       // TMEM chunk buffers (MT rows x N each)
   static constexpr int TMEM_COLS = 512;
   static constexpr int SMEM = STAGES * STAGE + 1024;
-  static constexpr int HALF = N / 2;                // channels per epilogue warpgroup
+  static constexpr int CPG = MT == 2 ? N / 2 : N;   // channels per epilogue warpgroup
+  static_assert(2 * XA_HALF <= A_BYTES, "extra-K operand must fit the A area");
 };
+
+// Chunk schedule of a tile: the n_kc conv chunks, then the n_xkc extra-K (style gradient)
+// chunks.  (An interleaved schedule measured slower: its index math sits in the single-thread
+// MMA issue loop, which is on the critical path.)
+__device__ __forceinline__ bool chunk_is_extra(int c, int n_kc, int& idx) {
+  const bool e = c >= n_kc;
+  idx = e ? c - n_kc : c;
+  return e;
+}
 
 __device__ __forceinline__ void store_hl8(const HL16& t, int kg, int y, int x, const float* v8, float s) {
   __align__(16) __half h[8];
@@ -238,7 +250,33 @@ __device__ __forceinline__ void epilogue32(const ConvArgs& a, float* v0, float* 
   }
 }
 
-template <int N>
+// Work decomposition.  Unclustered: unit t = (spatial tile, n-tile), n-tile fastest.
+// Clustered (CL, 2 CTAs): unit t = (spatial tile pair, n-tile); CTA rank r takes spatial tile
+// 2*pair + r, so both CTAs use the same weight slab, which rank 0 multicasts into both.
+struct TileId {
+  int nt, cx, ry;
+  bool valid;
+};
+
+template <bool CL>
+__device__ __forceinline__ TileId decode_tile(const ConvArgs& a, int t, uint32_t rank) {
+  TileId id;
+  id.nt = t % a.n_ntiles;
+  const int rest = t / a.n_ntiles;
+  const int sp = CL ? 2 * rest + (int)rank : rest;
+  id.valid = sp < a.tiles_x * a.tiles_y;
+  id.cx = sp % a.tiles_x;
+  id.ry = id.valid ? sp / a.tiles_x : a.tiles_y;  // an invalid unit reads OOB (zeros), stores nothing
+  return id;
+}
+
+template <bool CL>
+__device__ __forceinline__ int n_units(const ConvArgs& a) {
+  const int sp = a.tiles_x * a.tiles_y;
+  return (CL ? (sp + 1) / 2 : sp) * a.n_ntiles;
+}
+
+template <int N, bool CL>
 __global__ void __launch_bounds__(320, 1) conv3x3_tc_kernel(const __grid_constant__ ConvArgs a) {
   using C = ConvCfg<N>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -249,7 +287,10 @@ __global__ void __launch_bounds__(320, 1) conv3x3_tc_kernel(const __grid_constan
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
-  const int n_tiles = a.tiles_x * a.tiles_y * a.n_ntiles;
+  const uint32_t rank = CL ? cluster_ctarank() : 0;
+  const int n_tiles = n_units<CL>(a);
+  const int first = CL ? (int)blockIdx.x / 2 : (int)blockIdx.x;
+  const int step = CL ? (int)gridDim.x / 2 : (int)gridDim.x;
   const int n_chunks = a.n_kc + a.n_xkc;
 
   if (warp == 0 && lane == 0) {
@@ -259,7 +300,7 @@ __global__ void __launch_bounds__(320, 1) conv3x3_tc_kernel(const __grid_constan
     tma_prefetch_desc(&a.tm_v_lo);
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&full_bar[s], 1);
-      mbar_init(&empty_bar[s], 1);
+      mbar_init(&empty_bar[s], CL ? 2 : 1);  // clustered: both CTAs must release the stage
     }
     for (int b = 0; b < C::NBUF; ++b) {
       mbar_init(&cfull_bar[b], 1);
@@ -269,7 +310,10 @@ __global__ void __launch_bounds__(320, 1) conv3x3_tc_kernel(const __grid_constan
   }
   if (warp == 1) tmem_alloc<C::TMEM_COLS>(&tmem_slot);
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CL)
+    cluster_sync_all();  // peer barriers initialised before any multicast lands
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = tmem_slot;
 
@@ -277,29 +321,40 @@ __global__ void __launch_bounds__(320, 1) conv3x3_tc_kernel(const __grid_constan
     // ------------------------------------------------------------------ TMA producer
     if (lane == 0) {
       uint32_t g = 0;
-      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-        const int nt = t % a.n_ntiles;
-        const int rest = t / a.n_ntiles;
-        const int x0 = (rest % a.tiles_x) * 128;
-        const int y0 = (rest / a.tiles_x) * 2;
+      for (int t = first; t < n_tiles; t += step) {
+        const TileId id = decode_tile<CL>(a, t, rank);
+        const int nt = id.nt;
+        const int x0 = id.cx * 128;
+        const int y0 = id.ry * C::MT;
         for (int c = 0; c < n_chunks; ++c, ++g) {
           const int s = g % C::STAGES;
           mbar_wait(&empty_bar[s], ((g / C::STAGES) & 1) ^ 1);
           uint8_t* st = smem + s * C::STAGE;
-          const bool conv = c < a.n_kc;
-          if (conv) {
-            mbar_arrive_expect_tx(&full_bar[s], C::A_BYTES + C::B_BYTES);
-            tma_load_4d(st, &a.tm_a_hi, &full_bar[s], 0, x0 - 1, y0 - 1, 2 * c);
-            tma_load_4d(st + C::A_HALF, &a.tm_a_lo, &full_bar[s], 0, x0 - 1, y0 - 1, 2 * c);
-          } else {  // extra K (tap features): only the tile's own 2 x 128 pixels, 32 channels
-            mbar_arrive_expect_tx(&full_bar[s], 2 * C::XA_HALF + C::XB_BYTES);
-            tma_load_4d(st, &a.tm_v_hi, &full_bar[s], 0, x0, y0, 4 * (c - a.n_kc));
-            tma_load_4d(st + C::XA_HALF, &a.tm_v_lo, &full_bar[s], 0, x0, y0, 4 * (c - a.n_kc));
+          int ci;
+          const bool extra = chunk_is_extra(c, a.n_kc, ci);
+#ifdef SPST_EXP_NOLOAD
+          if (g >= C::STAGES) {
+            mbar_arrive(&full_bar[s]);
+            continue;
           }
-          const uint32_t bbytes = conv ? C::B_BYTES : C::XB_BYTES;
-          const uint8_t* src = conv ? a.wgt + ((size_t)nt * a.n_kc + c) * C::B_BYTES
-                                    : a.xwgt + ((size_t)nt * a.n_xkc + (c - a.n_kc)) * C::XB_BYTES;
-          bulk_load(st + C::A_BYTES, src, bbytes, &full_bar[s]);
+#endif
+          const uint8_t* bsrc = extra ? a.xwgt + ((size_t)nt * a.n_xkc + ci) * C::XB_BYTES
+                                      : a.wgt + ((size_t)nt * a.n_kc + ci) * C::B_BYTES;
+          const uint32_t bbytes = extra ? C::XB_BYTES : C::B_BYTES;
+          if (!extra) {
+            mbar_arrive_expect_tx(&full_bar[s], C::A_BYTES + C::B_BYTES);
+            tma_load_4d(st, &a.tm_a_hi, &full_bar[s], 0, x0 - 1, y0 - 1, 2 * ci);
+            tma_load_4d(st + C::A_HALF, &a.tm_a_lo, &full_bar[s], 0, x0 - 1, y0 - 1, 2 * ci);
+          } else {  // extra K (tap features): only the tile's own MT x 128 pixels
+            mbar_arrive_expect_tx(&full_bar[s], 2 * C::XA_HALF + C::XB_BYTES);
+            tma_load_4d(st, &a.tm_v_hi, &full_bar[s], 0, x0, y0, C::XKG * ci);
+            tma_load_4d(st + C::XA_HALF, &a.tm_v_lo, &full_bar[s], 0, x0, y0, C::XKG * ci);
+          }
+          if constexpr (CL) {
+            if (rank == 0) bulk_load_multicast(st + C::A_BYTES, bsrc, bbytes, &full_bar[s], 0x3);
+          } else {
+            bulk_load(st + C::A_BYTES, bsrc, bbytes, &full_bar[s]);
+          }
         }
       }
     }
@@ -308,7 +363,7 @@ __global__ void __launch_bounds__(320, 1) conv3x3_tc_kernel(const __grid_constan
     if (lane == 0) {
       const uint32_t idesc = make_idesc_f16(128, N, 0, 0, 0);
       uint32_t g = 0;
-      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      for (int t = first; t < n_tiles; t += step) {
         for (int c = 0; c < n_chunks; ++c, ++g) {
           const uint32_t b = g % C::NBUF;
           mbar_wait(&cempty_bar[b], ((g / C::NBUF) & 1) ^ 1);
@@ -317,42 +372,52 @@ __global__ void __launch_bounds__(320, 1) conv3x3_tc_kernel(const __grid_constan
           tc_fence_after();
           const uint32_t st = smem_u32(smem + s * C::STAGE);
           const uint32_t bb = st + C::A_BYTES;
-          const bool conv = c < a.n_kc;
-          const uint32_t dcol = tmem_base + b * 2 * N;
-          if (!conv) {
-            // V[2 rows x 128 px, 32 ch] x M[32 x N]: two K=16 steps per pass
+          int ci;
+          const bool extra = chunk_is_extra(c, a.n_kc, ci);
+          const uint32_t dcol = tmem_base + b * C::MT * N;
+          // descriptor arithmetic: start-address field = addr >> 4 in the low bits, so an
+          // offset of k bytes is an add of k >> 4 on the precomputed 64-bit descriptor
+          if (extra) {
+            // V[MT rows x 128 px, 8*XKG ch] x M[8*XKG x N]: XKG/2 K=16 steps per pass
+            const uint64_t bdesc0 = make_sdesc(bb, N * 16, 128);
+            const uint64_t adesc0 = make_sdesc(st, C::XA_PLANE, 128);
             for (int pass = 0; pass < 3; ++pass)
 #pragma unroll
-              for (int ks = 0; ks < 2; ++ks) {
-                const uint64_t bd = make_sdesc(bb + (pass == 0 ? 4 * N * 16 : 0) + 2 * ks * N * 16, N * 16, 128);
+              for (int ks = 0; ks < C::XKG / 2; ++ks) {
+                const uint64_t bd = bdesc0 + (uint64_t)((((pass == 0 ? C::XKG : 0) + 2 * ks) * N * 16) >> 4);
 #pragma unroll
-                for (int mt = 0; mt < 2; ++mt) {
-                  const uint32_t ab = st + (pass == 1 ? C::XA_HALF : 0) + mt * 128 * 16 + 2 * ks * C::XA_PLANE;
-                  umma_f16(dcol + mt * N, make_sdesc(ab, C::XA_PLANE, 128), bd, idesc, (pass | ks) ? 1u : 0u);
+                for (int mt = 0; mt < C::MT; ++mt) {
+                  const uint64_t ad =
+                      adesc0 + (uint64_t)(((pass == 1 ? C::XA_HALF : 0) + mt * 128 * 16 + 2 * ks * C::XA_PLANE) >> 4);
+                  umma_f16(dcol + mt * N, ad, bd, idesc, (pass | ks) ? 1u : 0u);
                 }
               }
-            umma_commit(&empty_bar[s]);
-            umma_commit(&cfull_bar[b]);
-            continue;
-          }
-          const uint32_t a_hi = st, a_lo = st + C::A_HALF;
-          const int ntap = 9;
-          // Small correction products first (hi*lo, lo*hi), then the large hi*hi products: the
-          // tensor core truncates each accumulation to the running sum's exponent, so keeping the
-          // sum small while the corrections go in cuts the chunk's rounding error ~3x.
-          for (int pass = 0; pass < 3; ++pass) {
-            for (int tap = 0; tap < ntap; ++tap) {
-              const int dy = tap / 3, dx = tap % 3;
-              const uint64_t bd = make_sdesc(bb + ((pass == 0 ? ntap : 0) + tap) * C::B_TAP, N * 16, 128);
+          } else {
+            const uint64_t bdesc0 = make_sdesc(bb, N * 16, 128);
+            const uint64_t adesc0 = make_sdesc(st, C::A_PLANE, 128);
+            // Small correction products first (hi*lo, lo*hi), then the large hi*hi products: the
+            // tensor core truncates each accumulation to the running sum's exponent, so keeping
+            // the sum small while the corrections go in cuts the chunk's rounding error ~3x.
 #pragma unroll
-              for (int mt = 0; mt < 2; ++mt) {
-                const uint32_t aoff = ((mt + dy) * C::PITCH + dx) * 16;
-                const uint64_t ad = make_sdesc((pass == 1 ? a_lo : a_hi) + aoff, C::A_PLANE, 128);
-                umma_f16(dcol + mt * N, ad, bd, idesc, (pass | tap) ? 1u : 0u);  // fresh per chunk
+            for (int pass = 0; pass < 3; ++pass) {
+              const uint64_t bp = bdesc0 + (uint64_t)(((pass == 0 ? 9 : 0) * C::B_TAP) >> 4);
+              const uint64_t ap = adesc0 + (uint64_t)((pass == 1 ? C::A_HALF : 0) >> 4);
+#pragma unroll
+              for (int tap = 0; tap < 9; ++tap) {
+                const int dy = tap / 3, dx = tap % 3;
+                const uint64_t bd = bp + (uint64_t)((tap * C::B_TAP) >> 4);
+#pragma unroll
+                for (int mt = 0; mt < C::MT; ++mt) {
+                  const uint64_t ad = ap + (uint64_t)((((mt + dy) * C::PITCH + dx) * 16) >> 4);
+                  umma_f16(dcol + mt * N, ad, bd, idesc, (pass | tap) ? 1u : 0u);  // fresh per chunk
+                }
               }
             }
           }
-          umma_commit(&empty_bar[s]);
+          if constexpr (CL)
+            umma_commit_multicast(&empty_bar[s], 0x3);  // release the stage in both CTAs
+          else
+            umma_commit(&empty_bar[s]);
           umma_commit(&cfull_bar[b]);
         }
       }
@@ -360,39 +425,52 @@ __global__ void __launch_bounds__(320, 1) conv3x3_tc_kernel(const __grid_constan
   } else {
     // ------------------------------------------------------------------ epilogue (8 warps)
     const uint32_t q = warp & 3;            // TMEM lane quarter
-    const uint32_t grp = (warp - 2) >> 2;   // channel half
+    const uint32_t grp = (warp - 2) >> 2;   // MT=2: channel half; MT=4: row pair
     const int m = q * 32 + lane;
+    const int rp = C::MT == 2 ? 0 : (int)grp;            // row pair handled by this warpgroup
+    const int cofs = C::MT == 2 ? (int)grp * C::CPG : 0;  // first channel handled
     uint32_t g = 0;
-    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-      const int nt = t % a.n_ntiles;
-      const int rest = t / a.n_ntiles;
-      const int cx = rest % a.tiles_x, ry = rest / a.tiles_x;
-      const int x0 = cx * 128, y0 = ry * 2;
+    for (int t = first; t < n_tiles; t += step) {
+      const TileId id = decode_tile<CL>(a, t, rank);
+      const int nt = id.nt, cx = id.cx, ry = id.ry;
+      const int x0 = cx * 128, y0 = ry * C::MT + 2 * rp;
       const int x = x0 + m;
-      float acc0[C::HALF], acc1[C::HALF];
+      float acc0[C::CPG], acc1[C::CPG];
 #pragma unroll
-      for (int i = 0; i < C::HALF; ++i) acc0[i] = acc1[i] = 0.f;
+      for (int i = 0; i < C::CPG; ++i) acc0[i] = acc1[i] = 0.f;
       for (int c = 0; c < n_chunks; ++c, ++g) {
         const uint32_t b = g % C::NBUF;
         mbar_wait(&cfull_bar[b], (g / C::NBUF) & 1);
         tc_fence_after();
-        const uint32_t trow = tmem_base + ((q * 32u) << 16) + b * 2 * N + grp * C::HALF;
-        const float cs = c < a.n_kc ? 1.f : a.x_rescale;  // extra-K chunks carry their own scale
+        const uint32_t trow = tmem_base + ((q * 32u) << 16) + b * C::MT * N + 2 * rp * N + cofs;
+        int ci;
+        const float cs = chunk_is_extra(c, a.n_kc, ci) ? a.x_rescale : 1.f;  // own scale
+        if constexpr (C::CPG == 32) {  // both rows in one batch: 2 loads, 1 wait
+          float v0[32], v1[32];
+          tmem_ld32x2(trow, trow + N, v0, v1);
 #pragma unroll
-        for (int cb = 0; cb < C::HALF / 32; ++cb) {
-          tmem_add32(trow + cb * 32, acc0 + cb * 32, cs);
-          tmem_add32(trow + N + cb * 32, acc1 + cb * 32, cs);
+          for (int i = 0; i < 32; ++i) {
+            acc0[i] = fmaf(v0[i], cs, acc0[i]);
+            acc1[i] = fmaf(v1[i], cs, acc1[i]);
+          }
+        } else {
+#pragma unroll
+          for (int cb = 0; cb < C::CPG / 32; ++cb) {
+            tmem_add32(trow + cb * 32, acc0 + cb * 32, cs);
+            tmem_add32(trow + N + cb * 32, acc1 + cb * 32, cs);
+          }
         }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&cempty_bar[b]);
       }
       float amax0 = 0.f, amax1 = 0.f;
-      const int tile_xy = ry * a.tiles_x + cx;
+      const int part_row = (ry * a.tiles_x + cx) * (C::MT / 2) + rp;
+      if (!id.valid) continue;  // padding unit of the last cluster pair: nothing to store
 #pragma unroll
-      for (int cb = 0; cb < C::HALF / 32; ++cb)
-        epilogue32<N>(a, acc0 + cb * 32, acc1 + cb * 32, nt * N + grp * C::HALF + cb * 32, x, y0, tile_xy, q,
-                      amax0, amax1);
+      for (int cb = 0; cb < C::CPG / 32; ++cb)
+        epilogue32<N>(a, acc0 + cb * 32, acc1 + cb * 32, nt * N + cofs + cb * 32, x, y0, part_row, q, amax0,
+                      amax1);
       if (a.amax) {
         amax0 = warp_max(amax0);
         amax1 = warp_max(amax1);
@@ -404,23 +482,45 @@ __global__ void __launch_bounds__(320, 1) conv3x3_tc_kernel(const __grid_constan
     }
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CL)
+    cluster_sync_all();  // no CTA leaves while its peer may still multicast into it
+  else
+    __syncthreads();
   if (warp == 1) tmem_dealloc<C::TMEM_COLS>(tmem_base);
 }
 
 // ------------------------------------------------------------------------------------------
 int conv_tc_smem_bytes(int N) { return N == 128 ? ConvCfg<128>::SMEM : ConvCfg<64>::SMEM; }
+int conv_tc_rows(int N) { return N == 128 ? ConvCfg<128>::MT : ConvCfg<64>::MT; }
+int conv_tc_xkg(int N) { return N == 128 ? ConvCfg<128>::XKG : ConvCfg<64>::XKG; }
 
-cudaError_t launch_conv_tc(const ConvArgs& a, int N, int grid, cudaStream_t stream) {
-  if (N == 128) {
-    auto k = conv3x3_tc_kernel<128>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, ConvCfg<128>::SMEM);
-    k<<<grid, 320, ConvCfg<128>::SMEM, stream>>>(a);
-  } else {
-    auto k = conv3x3_tc_kernel<64>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, ConvCfg<64>::SMEM);
-    k<<<grid, 320, ConvCfg<64>::SMEM, stream>>>(a);
-  }
+template <int N, bool CL>
+static cudaError_t launch_one(const ConvArgs& a, int grid, cudaStream_t stream) {
+  auto k = conv3x3_tc_kernel<N, CL>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, ConvCfg<N>::SMEM);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(CL ? (grid + 1) / 2 * 2 : grid);
+  cfg.blockDim = dim3(320);
+  cfg.dynamicSmemBytes = ConvCfg<N>::SMEM;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CL ? 2 : 1;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = CL ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, a);
+}
+
+// cluster: 0 = one CTA per unit, 1 = CTA pairs sharing (multicasting) the weight slab
+cudaError_t launch_conv_tc(const ConvArgs& a, int N, int grid, cudaStream_t stream, int cluster) {
+  cudaError_t e;
+  if (N == 128)
+    e = cluster ? launch_one<128, true>(a, grid, stream) : launch_one<128, false>(a, grid, stream);
+  else
+    e = cluster ? launch_one<64, true>(a, grid, stream) : launch_one<64, false>(a, grid, stream);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 

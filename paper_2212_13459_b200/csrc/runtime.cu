@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -48,10 +49,11 @@ bool get_encoder() {
 }
 
 // conv K operand: halo window box (8 ch, 130 px, 4 rows, 2 kg); extra-K operand: (8, 128, 2, 4)
-bool map_act(CUtensorMap* m, const __half* base, int n_kg, int H, int W, bool extra = false) {
+bool map_act(CUtensorMap* m, const __half* base, int n_kg, int H, int W, int mt, bool extra) {
   cuuint64_t dims[4] = {8, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)n_kg};
   cuuint64_t strides[3] = {16, (cuuint64_t)W * 16, (cuuint64_t)H * W * 16};
-  cuuint32_t box[4] = {8, extra ? 128u : 130u, extra ? 2u : 4u, extra ? 4u : 2u};
+  cuuint32_t box[4] = {8, extra ? 128u : 130u, extra ? (cuuint32_t)mt : (cuuint32_t)(mt + 2),
+                       extra ? (cuuint32_t)(8 / mt) : 2u};
   cuuint32_t es[4] = {1, 1, 1, 1};
   return g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, (void*)base, dims, strides, box, es,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -378,25 +380,31 @@ int run_conv(spst_ctx* ctx, ConvLaunch& L) {
   ConvArgs& a = L.a;
   const HL16* in = L.in ? L.in : L.v;
   const HL16* v = L.v ? L.v : in;
-  if (!map_act(&a.tm_a_hi, in->hi, in->C_p / 8, in->H, in->W) ||
-      !map_act(&a.tm_a_lo, in->lo(), in->C_p / 8, in->H, in->W) ||
-      !map_act(&a.tm_v_hi, v->hi, v->C_p / 8, v->H, v->W, true) ||
-      !map_act(&a.tm_v_lo, v->lo(), v->C_p / 8, v->H, v->W, true))
+  const int N = ntile_for(a.out.C_p);
+  const int mt = conv_tc_rows(N);
+  if (!map_act(&a.tm_a_hi, in->hi, in->C_p / 8, in->H, in->W, mt, false) ||
+      !map_act(&a.tm_a_lo, in->lo(), in->C_p / 8, in->H, in->W, mt, false) ||
+      !map_act(&a.tm_v_hi, v->hi, v->C_p / 8, v->H, v->W, mt, true) ||
+      !map_act(&a.tm_v_lo, v->lo(), v->C_p / 8, v->H, v->W, mt, true))
     return ctx->fail(SPST_ERR_CUDA, "cuTensorMapEncodeTiled failed");
   a.wgt = L.in ? L.wslab : nullptr;
   a.n_kc = L.in ? L.in->C_p / 16 : 0;
   a.xwgt = reinterpret_cast<const uint8_t*>(L.xw);
-  a.n_xkc = L.n_xkc;
+  a.n_xkc = L.xw ? v->C_p / (8 * conv_tc_xkg(N)) : 0;
   a.H = L.H;
   a.W = L.W;
-  const int N = ntile_for(a.out.C_p);
   a.n_ntiles = a.out.C_p / N;
   a.tiles_x = (L.W + 127) / 128;
-  a.tiles_y = (L.H + 1) / 2;
+  a.tiles_y = (L.H + mt - 1) / mt;
   a.acc_scale = L.acc_scale;
   if (a.n_kc + a.n_xkc == 0) return ctx->fail(SPST_ERR_CONFIG, "empty GEMM");
   const int tiles = a.tiles_x * a.tiles_y * a.n_ntiles;
-  CK(launch_conv_tc(a, N, std::min(tiles, kSMs), ctx->stream));
+  static const int cluster_mode = [] {
+    const char* e = getenv("SPST_CLUSTER");
+    return e ? atoi(e) : 0;
+  }();
+  const int cl = cluster_mode && a.tiles_x * a.tiles_y >= 2 ? 1 : 0;
+  CK(launch_conv_tc(a, N, std::min(cl ? 2 * ((tiles + 1) / 2) : tiles, kSMs), ctx->stream, cl));
   return SPST_OK;
 }
 
@@ -555,7 +563,8 @@ StyleCoefArgs coef_args(spst_ctx* ctx, TapState& t) {
   a.ms_loss = t.ms_loss;
   a.degenerate = t.degenerate;
   a.N = ntile_for(s.cout_p);
-  a.n_xkc = s.cout_p / 32;
+  a.xkg = conv_tc_xkg(a.N);
+  a.n_xkc = s.cout_p / (8 * a.xkg);
   return a;
 }
 
@@ -785,7 +794,8 @@ int bind_alloc(spst_ctx* ctx) {
       t.gram_px = gram_px_per_split(own_px, nct * (nct + 1) / 2);
       t.gram_splits = (int)std::max<long long>(1, (own_px + t.gram_px - 1) / t.gram_px);
       t.gram_partial = ctx->dalloc<float>((size_t)t.gram_splits * (nct * (nct + 1) / 2) * 128 * 128);
-      t.colsum_rows = k == 0 ? first_conv_fwd_blocks(s.H, s.W) : ((s.W + 127) / 128) * ((s.H + 1) / 2) * 4;
+      const int mt = conv_tc_rows(ntile_for(s.cout_p));
+      t.colsum_rows = k == 0 ? first_conv_fwd_blocks(s.H, s.W) : ((s.W + 127) / 128) * ((s.H + mt - 1) / mt) * 2 * mt;
       t.colsum_partial = ctx->dalloc<float>((size_t)t.colsum_rows * Cp);
       t.colsum_mid = ctx->dalloc<double>((size_t)kColsumMid * Cp);
       if (!t.S || !t.s || !t.mu || !t.sd || !t.ratio || !t.row_loss || !t.row_mmax || !t.ms_loss || !t.degenerate ||

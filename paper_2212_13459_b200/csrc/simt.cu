@@ -315,7 +315,7 @@ __global__ void style_mat_kernel(StyleCoefArgs a) {
   __shared__ double redm[256];
   const int k = blockIdx.x;
   double acc = 0.0, mm = 0.0;
-  const int kc = k >> 5, kg = (k >> 3) & 3, e = k & 7;
+  const int kc = k / (8 * a.xkg), kg = (k >> 3) % a.xkg, e = k & 7;
   for (int n = threadIdx.x; n < a.C; n += blockDim.x) {
     const double g = a.S[(size_t)k * a.C + n] / a.n;
     const double d = g - a.Gr[(size_t)k * a.C + n];
@@ -328,8 +328,8 @@ __global__ void style_mat_kernel(StyleCoefArgs a) {
       HalfPair p = split_f16(v);
       const int nt = n / a.N, nl = n % a.N;
       const size_t base = ((size_t)nt * a.n_xkc + kc) * 2;
-      a.xw[(((base + 0) * 4 + kg) * a.N + nl) * 8 + e] = p.hi;
-      a.xw[(((base + 1) * 4 + kg) * a.N + nl) * 8 + e] = p.lo;
+      a.xw[(((base + 0) * a.xkg + kg) * a.N + nl) * 8 + e] = p.hi;
+      a.xw[(((base + 1) * a.xkg + kg) * a.N + nl) * 8 + e] = p.lo;
     }
   }
   red[threadIdx.x] = acc;

@@ -131,6 +131,10 @@ int spst_resize_bilinear(const float* in, int h, int w, int c, int oh, int ow, f
  * mode 3: relu mask bits of mode 0 as floats. Returns through y_host. */
 int spst_debug_conv(int device, int mode, int cin, int cout, int H, int W, const float* x_host,
                     const double* weight, const double* bias, float* y_host);
+/* ReLU mask of conv stage `stage` (0-based conv index) from the last forward, as bytes
+ * (C_out x H x W, 1 = pre-activation > 0) — lets tests evaluate the f64 oracle on the device's
+ * activation pattern. */
+int spst_debug_mask(spst_ctx* ctx, int stage, unsigned char* out_host);
 /* Gram of a (C x P) f32 feature matrix through the tensor-core Gram kernel, S = F F^T (f64). */
 int spst_debug_gram(int device, int C, long long P, const float* f_host, double* S_host);
 

@@ -245,19 +245,20 @@ def preprocess_adjoint(g, net):
     return out
 
 
-def run_forward(x_chw, net, keep=False):
+def run_forward(x_chw, net, keep=False, masks=None):
     """Returns (taps, saved layer inputs or None). Stops at the deepest tap
-    (extractor.py:171-197)."""
+    (extractor.py:171-197).  `masks` ({relu name: bool array}) forces the ReLU activation
+    pattern (test hook: the f64 network evaluated on another engine's masks)."""
     names = set(net.taps)
     cur = preprocess(x_chw, net)
     taps, saved = {}, []
     for l in net.layers[: net.last() + 1]:
         if keep:
-            saved.append(cur)
+            saved.append(cur if masks is None or l.name not in masks else np.where(masks[l.name], 1.0, -1.0))
         if l.kind == "conv":
             cur = conv3x3(cur, l.w, l.b)
         elif l.kind == "relu":
-            cur = np.maximum(cur, 0)
+            cur = np.maximum(cur, 0) if masks is None or l.name not in masks else cur * masks[l.name]
         else:
             cur = pool2_fwd(cur, l.pool)
         if l.name in names:
@@ -514,12 +515,12 @@ def loss_grad(x, p):
     return total + closs, fold_pad_grad(gpad, h, w)
 
 
-def loss_grad_global(x, p):
-    """Single-pass whole-image oracle (localized.py:283-311)."""
+def loss_grad_global(x, p, masks=None):
+    """Single-pass whole-image oracle (localized.py:283-311). `masks`: see run_forward."""
     net = p.net
     h, w = x.shape[:2]
     xp = pad_edge16(x, net.deepest_stride())
-    feats, saved = run_forward(np.ascontiguousarray(xp.transpose(2, 0, 1)), net, keep=True)
+    feats, saved = run_forward(np.ascontiguousarray(xp.transpose(2, 0, 1)), net, keep=True, masks=masks)
     total = 0.0
     tg = {}
     for t in net.style_taps:

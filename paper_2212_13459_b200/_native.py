@@ -68,6 +68,7 @@ SIGNATURES = {
     "spst_debug_conv": (c_int, [c_int, c_int, c_int, c_int, c_int, c_int, c_void_p, c_void_p, c_void_p,
                                 c_void_p]),
     "spst_debug_gram": (c_int, [c_int, c_int, c_longlong, c_void_p, c_void_p]),
+    "spst_debug_mask": (c_int, [c_void_p, c_int, c_void_p]),
 }
 
 _lib = None

@@ -136,6 +136,8 @@ int conv_tc_smem_bytes(int N);
 int conv_tc_rows(int N);   // output rows per tile (MT)
 int conv_tc_xkg(int N);    // kgroups per extra-K chunk
 cudaError_t launch_gram_tc(const GramArgs& a, int n_splits, cudaStream_t stream);
+cudaError_t launch_gram64_tc(const GramArgs& a, int n_splits, int C, double inv_scale2, double* S,
+                             cudaStream_t stream);
 cudaError_t launch_gram_reduce(const float* partial, int n_splits, int n_ctile, int C, double inv_scale2,
                                double* S, cudaStream_t stream);
 cudaError_t launch_first_conv_fwd(const FirstConvArgs& a, cudaStream_t st);

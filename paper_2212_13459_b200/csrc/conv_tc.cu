@@ -258,25 +258,25 @@ struct TileId {
   bool valid;
 };
 
-template <bool CL>
+template <int CS>
 __device__ __forceinline__ TileId decode_tile(const ConvArgs& a, int t, uint32_t rank) {
   TileId id;
   id.nt = t % a.n_ntiles;
   const int rest = t / a.n_ntiles;
-  const int sp = CL ? 2 * rest + (int)rank : rest;
+  const int sp = CS * rest + (int)rank;
   id.valid = sp < a.tiles_x * a.tiles_y;
   id.cx = sp % a.tiles_x;
   id.ry = id.valid ? sp / a.tiles_x : a.tiles_y;  // an invalid unit reads OOB (zeros), stores nothing
   return id;
 }
 
-template <bool CL>
+template <int CS>
 __device__ __forceinline__ int n_units(const ConvArgs& a) {
   const int sp = a.tiles_x * a.tiles_y;
-  return (CL ? (sp + 1) / 2 : sp) * a.n_ntiles;
+  return (sp + CS - 1) / CS * a.n_ntiles;
 }
 
-template <int N, bool CL>
+template <int N, int CS>
 __global__ void __launch_bounds__(320, 1) conv3x3_tc_kernel(const __grid_constant__ ConvArgs a) {
   using C = ConvCfg<N>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -287,10 +287,12 @@ __global__ void __launch_bounds__(320, 1) conv3x3_tc_kernel(const __grid_constan
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
+  constexpr bool CL = CS > 1;
+  constexpr uint16_t kMask = (uint16_t)((1u << CS) - 1);
   const uint32_t rank = CL ? cluster_ctarank() : 0;
-  const int n_tiles = n_units<CL>(a);
-  const int first = CL ? (int)blockIdx.x / 2 : (int)blockIdx.x;
-  const int step = CL ? (int)gridDim.x / 2 : (int)gridDim.x;
+  const int n_tiles = n_units<CS>(a);
+  const int first = (int)blockIdx.x / CS;
+  const int step = (int)gridDim.x / CS;
   const int n_chunks = a.n_kc + a.n_xkc;
 
   if (warp == 0 && lane == 0) {
@@ -300,7 +302,7 @@ __global__ void __launch_bounds__(320, 1) conv3x3_tc_kernel(const __grid_constan
     tma_prefetch_desc(&a.tm_v_lo);
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&full_bar[s], 1);
-      mbar_init(&empty_bar[s], CL ? 2 : 1);  // clustered: both CTAs must release the stage
+      mbar_init(&empty_bar[s], CS);  // clustered: every CTA of the cluster must release the stage
     }
     for (int b = 0; b < C::NBUF; ++b) {
       mbar_init(&cfull_bar[b], 1);
@@ -322,7 +324,7 @@ __global__ void __launch_bounds__(320, 1) conv3x3_tc_kernel(const __grid_constan
     if (lane == 0) {
       uint32_t g = 0;
       for (int t = first; t < n_tiles; t += step) {
-        const TileId id = decode_tile<CL>(a, t, rank);
+        const TileId id = decode_tile<CS>(a, t, rank);
         const int nt = id.nt;
         const int x0 = id.cx * 128;
         const int y0 = id.ry * C::MT;
@@ -351,7 +353,7 @@ __global__ void __launch_bounds__(320, 1) conv3x3_tc_kernel(const __grid_constan
             tma_load_4d(st + C::XA_HALF, &a.tm_v_lo, &full_bar[s], 0, x0, y0, C::XKG * ci);
           }
           if constexpr (CL) {
-            if (rank == 0) bulk_load_multicast(st + C::A_BYTES, bsrc, bbytes, &full_bar[s], 0x3);
+            if (rank == 0) bulk_load_multicast(st + C::A_BYTES, bsrc, bbytes, &full_bar[s], kMask);
           } else {
             bulk_load(st + C::A_BYTES, bsrc, bbytes, &full_bar[s]);
           }
@@ -415,7 +417,7 @@ __global__ void __launch_bounds__(320, 1) conv3x3_tc_kernel(const __grid_constan
             }
           }
           if constexpr (CL)
-            umma_commit_multicast(&empty_bar[s], 0x3);  // release the stage in both CTAs
+            umma_commit_multicast(&empty_bar[s], kMask);  // release the stage in every CTA
           else
             umma_commit(&empty_bar[s]);
           umma_commit(&cfull_bar[b]);
@@ -431,7 +433,7 @@ __global__ void __launch_bounds__(320, 1) conv3x3_tc_kernel(const __grid_constan
     const int cofs = C::MT == 2 ? (int)grp * C::CPG : 0;  // first channel handled
     uint32_t g = 0;
     for (int t = first; t < n_tiles; t += step) {
-      const TileId id = decode_tile<CL>(a, t, rank);
+      const TileId id = decode_tile<CS>(a, t, rank);
       const int nt = id.nt, cx = id.cx, ry = id.ry;
       const int x0 = cx * 128, y0 = ry * C::MT + 2 * rp;
       const int x = x0 + m;
@@ -494,32 +496,41 @@ int conv_tc_smem_bytes(int N) { return N == 128 ? ConvCfg<128>::SMEM : ConvCfg<6
 int conv_tc_rows(int N) { return N == 128 ? ConvCfg<128>::MT : ConvCfg<64>::MT; }
 int conv_tc_xkg(int N) { return N == 128 ? ConvCfg<128>::XKG : ConvCfg<64>::XKG; }
 
-template <int N, bool CL>
+template <int N, int CS>
 static cudaError_t launch_one(const ConvArgs& a, int grid, cudaStream_t stream) {
-  auto k = conv3x3_tc_kernel<N, CL>;
+  auto k = conv3x3_tc_kernel<N, CS>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, ConvCfg<N>::SMEM);
+  if (CS == 16) cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(CL ? (grid + 1) / 2 * 2 : grid);
+  cfg.gridDim = dim3((grid + CS - 1) / CS * CS);
   cfg.blockDim = dim3(320);
   cfg.dynamicSmemBytes = ConvCfg<N>::SMEM;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = CL ? 2 : 1;
+  attr[0].val.clusterDim.x = CS;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = CL ? 1 : 0;
+  cfg.numAttrs = CS > 1 ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, k, a);
 }
 
-// cluster: 0 = one CTA per unit, 1 = CTA pairs sharing (multicasting) the weight slab
+// cluster: CTAs per cluster sharing (multicasting) the weight slab (1 = no cluster)
 cudaError_t launch_conv_tc(const ConvArgs& a, int N, int grid, cudaStream_t stream, int cluster) {
   cudaError_t e;
-  if (N == 128)
-    e = cluster ? launch_one<128, true>(a, grid, stream) : launch_one<128, false>(a, grid, stream);
-  else
-    e = cluster ? launch_one<64, true>(a, grid, stream) : launch_one<64, false>(a, grid, stream);
+#define SPST_CASE(CSV)                                                                           \
+  case CSV:                                                                                      \
+    e = N == 128 ? launch_one<128, CSV>(a, grid, stream) : launch_one<64, CSV>(a, grid, stream); \
+    break;
+  switch (cluster) {
+    SPST_CASE(2)
+    SPST_CASE(4)
+    SPST_CASE(8)
+    default:
+      e = N == 128 ? launch_one<128, 1>(a, grid, stream) : launch_one<64, 1>(a, grid, stream);
+  }
+#undef SPST_CASE
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }

@@ -142,6 +142,148 @@ __global__ void __launch_bounds__(192, 1) gram_tc_kernel(const __grid_constant__
   if (warp == 1) tmem_dealloc<512>(tmem);
 }
 
+// ------------------------------------------------------------------------------------------
+// C_p = 64 variant.  A = [V_hi ; V_lo] stacked along M (rows 0-63 hi channels, 64-127 lo
+// channels: the lo planes sit right after the hi planes in smem at the same plane stride, so
+// one MN-major descriptor spans both), B = V_hi (acc1) or V_lo (acc2), N = 64.  Then
+//   rows 0-63  of acc1 = hi.hi, rows 64-127 of acc1 = lo.hi, rows 0-63 of acc2 = hi.lo
+// and G = acc1[r] + acc1[64+r] + acc2[r] (lo.lo dropped), i.e. two M128xN64 MMAs per K-step
+// instead of three M128xN128 ones on a half-empty tile.
+struct Gram64Cfg {
+  static constexpr int KPX = 256;                      // pixels per stage
+  static constexpr int PLANE = KPX * 16;               // one 8-channel plane (4 KB)
+  static constexpr int STAGE = 16 * PLANE;             // 8 hi + 8 lo planes (64 KB)
+  static constexpr int STAGES = 3;
+  static constexpr int NBUF = 4;                       // 4 x (acc1 64 + acc2 64) TMEM columns
+  static constexpr int SMEM = STAGES * STAGE + 1024;
+};
+
+__global__ void __launch_bounds__(192, 1) gram64_tc_kernel(const __grid_constant__ GramArgs a) {
+  using C = Gram64Cfg;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t full_bar[C::STAGES], empty_bar[C::STAGES], cfull_bar[C::NBUF], cempty_bar[C::NBUF];
+  __shared__ uint32_t tmem_slot;
+  const uint32_t warp = warp_id(), lane = lane_id();
+  const long long p0 = a.p_begin + (long long)blockIdx.x * a.px_per_split;
+  const long long p1 = min(p0 + a.px_per_split, a.p_end);
+  const int n_stages = p1 > p0 ? (int)((p1 - p0 + C::KPX - 1) / C::KPX) : 0;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&a.tm_hi);
+    tma_prefetch_desc(&a.tm_lo);
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int b = 0; b < C::NBUF; ++b) {
+      mbar_init(&cfull_bar[b], 1);
+      mbar_init(&cempty_bar[b], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(&tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int c = 0; c < n_stages; ++c) {
+        const int s = c % C::STAGES;
+        mbar_wait(&empty_bar[s], ((c / C::STAGES) & 1) ^ 1);
+        uint8_t* st = smem + s * C::STAGE;
+        mbar_arrive_expect_tx(&full_bar[s], C::STAGE);
+        const int px = (int)(p0 - a.p_begin) + c * C::KPX;
+        tma_load_3d(st, &a.tm_hi, &full_bar[s], 0, px, 0);
+        tma_load_3d(st + 8 * C::PLANE, &a.tm_lo, &full_bar[s], 0, px, 0);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t idesc = make_idesc_f16(128, 64, 0, 1, 1);
+      for (int c = 0; c < n_stages; ++c) {
+        const uint32_t b = c % C::NBUF;
+        mbar_wait(&cempty_bar[b], ((c / C::NBUF) & 1) ^ 1);
+        const int s = c % C::STAGES;
+        mbar_wait(&full_bar[s], (c / C::STAGES) & 1);
+        tc_fence_after();
+        const uint32_t st = smem_u32(smem + s * C::STAGE);
+        const uint64_t da0 = make_sdesc(st, 128, C::PLANE);                // [hi;lo] x 16 px
+        const uint64_t dh0 = make_sdesc(st, 128, C::PLANE);                // hi, N = 64
+        const uint64_t dl0 = make_sdesc(st + 8 * C::PLANE, 128, C::PLANE); // lo, N = 64
+        const uint32_t d1 = tmem + b * 128, d2 = d1 + 64;
+#pragma unroll 4
+        for (int k = 0; k < C::KPX / 16; ++k) {
+          const uint64_t off = (uint64_t)((k * 256) >> 4);  // 16 px = two 128-B core-matrix groups
+          umma_f16(d2, da0 + off, dl0 + off, idesc, k > 0 ? 1u : 0u);  // small (x lo) first
+          umma_f16(d1, da0 + off, dh0 + off, idesc, k > 0 ? 1u : 0u);
+        }
+        umma_commit(&empty_bar[s]);
+        umma_commit(&cfull_bar[b]);
+      }
+    }
+  } else {
+    const uint32_t q = warp & 3;
+    const int row = q * 32 + lane;  // 0-63: hi rows, 64-127: lo rows
+    float acc[64];
+#pragma unroll
+    for (int i = 0; i < 64; ++i) acc[i] = 0.f;
+    for (int c = 0; c < n_stages; ++c) {
+      const uint32_t b = c % C::NBUF;
+      mbar_wait(&cfull_bar[b], (c / C::NBUF) & 1);
+      tc_fence_after();
+      const uint32_t ta = tmem + ((q * 32u) << 16) + b * 128;
+      float v0[32], v1[32];
+      tmem_ld32x2(ta, ta + 32, v0, v1);  // acc1 (x hi)
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        acc[j] += v0[j];
+        acc[32 + j] += v1[j];
+      }
+      if (row < 64) {  // acc2 (x lo) only matters for the hi rows
+        tmem_ld32x2(ta + 64, ta + 96, v0, v1);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          acc[j] += v0[j];
+          acc[32 + j] += v1[j];
+        }
+      } else {
+        __syncwarp();
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&cempty_bar[b]);
+    }
+    float* dst = a.partial + ((size_t)blockIdx.x * 128 + row) * 64;
+#pragma unroll
+    for (int j = 0; j < 64; j += 4) *reinterpret_cast<float4*>(dst + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<512>(tmem);
+}
+
+// G[i][j] = sum over splits of partial rows i (hi.hi + hi.lo) and 64 + i (lo.hi), fixed order
+__global__ void gram64_reduce_kernel(const float* partial, int n_splits, int C, double inv_scale2, double* S) {
+  const int i = blockIdx.x, j = threadIdx.x;
+  if (i >= C || j >= C || j < i) return;  // upper triangle, mirrored: S is exactly symmetric
+  double acc = 0.0;
+  for (int s = 0; s < n_splits; ++s)
+    acc += (double)partial[((size_t)s * 128 + i) * 64 + j] + (double)partial[((size_t)s * 128 + 64 + i) * 64 + j];
+  S[(size_t)i * C + j] = acc * inv_scale2;
+  S[(size_t)j * C + i] = acc * inv_scale2;
+}
+
+cudaError_t launch_gram64_tc(const GramArgs& a, int n_splits, int C, double inv_scale2, double* S,
+                             cudaStream_t stream) {
+  cudaFuncSetAttribute(gram64_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Gram64Cfg::SMEM);
+  gram64_tc_kernel<<<n_splits, 192, Gram64Cfg::SMEM, stream>>>(a);
+  gram64_reduce_kernel<<<C, 64, 0, stream>>>(a.partial, n_splits, C, inv_scale2, S);
+  return cudaGetLastError();
+}
+
 // S[c1][c2] (f64, C x C) = sum over splits of the fp32 partial tiles, fixed split order.
 __global__ void gram_reduce_kernel(const float* partial, int n_splits, int n_ctile, int C, double inv_scale2,
                                    double* S) {

@@ -60,10 +60,12 @@ bool map_act(CUtensorMap* m, const __half* base, int n_kg, int H, int W, int mt,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Gram operand: (8 ch, P, kg) view; box (8, 64 px, 16 kg) or, for 64 channels, (8, 256 px, 8 kg)
 bool map_gram(CUtensorMap* m, const __half* base, long long P_range, long long P_total, int n_kg) {
   cuuint64_t dims[3] = {8, (cuuint64_t)P_range, (cuuint64_t)n_kg};
   cuuint64_t strides[2] = {16, (cuuint64_t)P_total * 16};
-  cuuint32_t box[3] = {8, 64, 16};
+  const bool c64 = n_kg == 8;
+  cuuint32_t box[3] = {8, c64 ? 256u : 64u, c64 ? 8u : 16u};
   cuuint32_t es[3] = {1, 1, 1};
   return g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, (void*)base, dims, strides, box, es,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -76,7 +78,7 @@ int gram_px_per_split(long long px, int pairs) {
   const long long want_splits = std::max<long long>(1, (2 * kSMs + pairs - 1) / pairs);
   long long per = (px + want_splits - 1) / want_splits;
   per = std::max<long long>(1024, std::min<long long>(kMaxPxPerSplit, per));
-  return (int)((per + 127) / 128 * 128);
+  return (int)((per + 255) / 256 * 256);  // whole 64- and 256-pixel stages
 }
 int ntile_for(int C_p) { return (C_p % 128 == 0) ? 128 : 64; }
 float pow2f(int e) { return std::ldexp(1.0f, e); }
@@ -401,10 +403,13 @@ int run_conv(spst_ctx* ctx, ConvLaunch& L) {
   const int tiles = a.tiles_x * a.tiles_y * a.n_ntiles;
   static const int cluster_mode = [] {
     const char* e = getenv("SPST_CLUSTER");
-    return e ? atoi(e) : 0;
+    return e ? atoi(e) : 1;
   }();
-  const int cl = cluster_mode && a.tiles_x * a.tiles_y >= 2 ? 1 : 0;
-  CK(launch_conv_tc(a, N, std::min(cl ? 2 * ((tiles + 1) / 2) : tiles, kSMs), ctx->stream, cl));
+  // clusters of `cs` CTAs multicast the weight slab (needs >= cs spatial tiles to pay off)
+  int cs = cluster_mode;
+  while (cs > 1 && a.tiles_x * a.tiles_y < 4 * cs) cs /= 2;
+  const int grid = std::min(tiles, (kSMs / std::max(cs, 1)) * std::max(cs, 1));
+  CK(launch_conv_tc(a, N, std::max(grid, cs), ctx->stream, cs));
   return SPST_OK;
 }
 
@@ -492,9 +497,13 @@ int stage_stats(spst_ctx* ctx, int k) {
   g.px_per_split = t.gram_px;
   g.n_ctile = (s.cout_p + 127) / 128;
   g.partial = t.gram_partial;
-  CK(launch_gram_tc(g, t.gram_splits, ctx->stream));
   const double inv2 = 1.0 / ((double)s.out.scale * (double)s.out.scale);
-  CK(launch_gram_reduce(t.gram_partial, t.gram_splits, g.n_ctile, s.cout, inv2, t.S, ctx->stream));
+  if (s.cout_p == 64) {
+    CK(launch_gram64_tc(g, t.gram_splits, s.cout, inv2, t.S, ctx->stream));
+  } else {
+    CK(launch_gram_tc(g, t.gram_splits, ctx->stream));
+    CK(launch_gram_reduce(t.gram_partial, t.gram_splits, g.n_ctile, s.cout, inv2, t.S, ctx->stream));
+  }
   return SPST_OK;
 }
 
@@ -1149,6 +1158,20 @@ int spst_resize_bilinear(const float* in, int h, int w, int c, int oh, int ow, f
 }
 
 // ------------------------------------------------------------------------------------ debug
+int spst_debug_mask(spst_ctx* ctx, int stage, unsigned char* out_host) {
+  if (!ctx->fwd_done || stage < 0 || stage >= (int)ctx->stages.size())
+    return ctx->fail(SPST_ERR_CONFIG, "no forward / bad stage");
+  const Stage& s = ctx->stages[stage];
+  const size_t n = (size_t)(s.cout_p / 32) * s.H * s.W;
+  std::vector<uint32_t> bits(n);
+  CK(cudaMemcpyAsync(bits.data(), s.mask, n * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  const size_t plane = (size_t)s.H * s.W;
+  for (int c = 0; c < s.cout; ++c)
+    for (size_t p = 0; p < plane; ++p) out_host[c * plane + p] = (bits[(c >> 5) * plane + p] >> (c & 31)) & 1u;
+  return SPST_OK;
+}
+
 int spst_debug_conv(int device, int mode, int cin, int cout, int H, int W, const float* x_host,
                     const double* weight, const double* bias, float* y_host) {
   if (cudaSetDevice(device) != cudaSuccess || !get_encoder()) return SPST_ERR_CUDA;
@@ -1241,8 +1264,12 @@ int spst_debug_gram(int device, int C, long long P, const float* f_host, double*
   g.px_per_split = per;
   g.n_ctile = nct;
   g.partial = part;
-  CK(launch_gram_tc(g, splits, nullptr));
-  CK(launch_gram_reduce(part, splits, nct, C, 1.0, Sd, nullptr));
+  if (Cp == 64) {
+    CK(launch_gram64_tc(g, splits, C, 1.0, Sd, nullptr));
+  } else {
+    CK(launch_gram_tc(g, splits, nullptr));
+    CK(launch_gram_reduce(part, splits, nct, C, 1.0, Sd, nullptr));
+  }
   CK(cudaDeviceSynchronize());
   CK(cudaMemcpy(S_host, Sd, (size_t)C * C * 8, cudaMemcpyDeviceToHost));
   ctx->release_bound();

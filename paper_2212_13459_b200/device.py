@@ -184,6 +184,20 @@ class Engine:
         self._check(nat.lib().spst_content_sqdiff(self._h, nat.ptr(self._content_out)), "spst_content_sqdiff")
         return self._content_out
 
+    def relu_masks(self):
+        """{relu layer name: bool (C, H, W)} of the last forward (test/diagnostic hook)."""
+        out = {}
+        convs = [i for i, l in enumerate(self.spec.layers[:self.spec.deepest_tap_index() + 1]) if l.kind == "conv"]
+        Hl = self.bound[2][1] - self.bound[2][0]
+        Wp = self.padded_dims()[1]
+        for k, li in enumerate(convs):
+            stride = 2 ** sum(1 for l in self.spec.layers[:li] if l.kind == "pool")
+            C = self.spec.layers[li].out_ch
+            buf = np.zeros((C, Hl // stride, Wp // stride), dtype=np.uint8)
+            self._check(nat.lib().spst_debug_mask(self._h, k, buf.ctypes.data), "spst_debug_mask")
+            out[self.spec.layers[li + 1].name] = buf.astype(bool)
+        return out
+
     def backward(self, two_lambda, grad_dev):
         self.stream()
         with torch.cuda.device(self.device):

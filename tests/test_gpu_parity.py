@@ -163,21 +163,35 @@ def test_vgg19_lbfgs_same_x_first_five_iterates(vgg_spec, vgg_c1):
     po = O.build_problem(d["c1_u"].astype(np.float64), d["c1_v"].astype(np.float64), net,
                          O.default_weights(net, lam), 512, 256)
     po32 = O.build_problem(d["c1_u"], d["c1_v"], net, O.default_weights(net, lam), 512, 256)
-    errs = []
+    errs, gaps = [], []
     for it, xi in enumerate(iterates, start=1):
         lo, go = O.loss_grad_global(xi.astype(np.float64), po)
         _, g32 = O.loss_grad_global(xi, po32)
         loss, g = spst.loss_grad(xi, p)
-        err, gap = rel_l2(g, go), rel_l2(g32, go)
+        # the f64 network evaluated on OUR activation pattern: isolates arithmetic from flips
+        masks = p.engine.relu_masks()
+        lm, gm = O.loss_grad_global(xi.astype(np.float64), po, masks=masks)
+        flips = sum(int(np.sum(masks[t] != (m_ > 0))) for t, m_ in _f64_preacts(po, xi).items())
+        err, gap, arith = rel_l2(g, go), rel_l2(g32, go), rel_l2(g, gm)
         errs.append(err)
-        print(f"iterate {it}: loss rel {abs(loss - lo) / lo:.2e}, grad rel-L2 {err:.2e} (oracle-f32 gap {gap:.2e})")
+        gaps.append(gap)
+        print(f"iterate {it}: loss rel {abs(loss - lo) / lo:.2e}, grad rel-L2 vs f64 {err:.2e} "
+              f"(oracle-f32 {gap:.2e}); vs f64-on-our-masks {arith:.2e}; ReLU flips {flips}")
         assert abs(loss - lo) <= 1e-4 * lo
-    # The gradient is discontinuous at ReLU boundaries: an fp32-class forward flips a mask
-    # wherever |pre-activation| is below its rounding error (SURVEY.md §0 finding 2).  The bar:
-    # median over the five iterates within 1e-3, every iterate within 5e-3 (measured: the
-    # reference-class f32 path itself reaches 1-2.6e-3 on some of these iterates).
-    assert float(np.median(errs)) <= 1e-3
+        assert abs(loss - lm) <= 1e-4 * lm
+        assert arith <= 1e-4          # arithmetic: fp32-class
+    # The plain comparison carries the ReLU-flip lottery (SURVEY.md §0 finding 2); require it to
+    # stay within the reference-class f32 envelope: mean error <= 2x the oracle-f32 mean + 5e-4.
+    assert float(np.mean(errs)) <= 2 * float(np.mean(gaps)) + 5e-4
     assert max(errs) <= 5e-3
+
+
+def _f64_preacts(po, xi):
+    """f64 pre-activations of every ReLU at x (for counting mask flips)."""
+    net = po.net
+    xp = O.pad_edge16(xi.astype(np.float64), net.deepest_stride())
+    _, saved = O.run_forward(np.ascontiguousarray(xp.transpose(2, 0, 1)), net, keep=True)
+    return {l.name: saved[i] for i, l in enumerate(net.layers[:net.last() + 1]) if l.kind == "relu"}
 
 
 # ---------------------------------------------------------------- L-BFGS semantics on device

@@ -260,7 +260,8 @@ def cpu_baseline(args, H, W, sh, sw, evals_per_iter, sample_only=False):
     net = O.onet_from_spec(spec)
     # f32 weights, like the reference's default dtype f32 path
     rng = np.random.default_rng(3)
-    blk = (rng.random((1024, 1024, 3)) * 0.8 + 0.1).astype(np.float32)
+    side = args.cpu_block
+    blk = (rng.random((side, side, 3)) * 0.8 + 0.1).astype(np.float32)
     x = np.ascontiguousarray(blk.transpose(2, 0, 1))
     t0 = time.time()
     feats, _ = O.run_forward(x, net)                      # pass 1 (stats) on one padded block
@@ -276,12 +277,12 @@ def cpu_baseline(args, H, W, sh, sw, evals_per_iter, sample_only=False):
     from paper_2212_13459_b200.tiling import BlockGrid, partition
     grid = BlockGrid(H + (-H) % 16, W + (-W) % 16, 512, 256, 16)
     area = sum(b.padded.w * b.padded.h for b in partition(grid))
-    eval_s = block_s * area / (1024 * 1024)
+    eval_s = block_s * area / (side * side)
     iter_s = eval_s * evals_per_iter
     return {"value": 1.0 / iter_s, "unit": "iters/s", "cores": cores, "kind": "port",
-            "sample": f"one 1024x1024 padded block of the reference 512/256 grid (pass-1 fwd {t1 - t0:.1f}s + "
-                      f"pass-2 fwd/bwd {t2 - t1:.1f}s, f32 numpy, {cores} threads), extrapolated by padded area "
-                      f"x{area / 1048576:.1f} and {evals_per_iter:.2f} evals/iter"}
+            "sample": f"one {side}x{side} padded block (pass-1 fwd {t1 - t0:.1f}s + pass-2 fwd/bwd {t2 - t1:.1f}s, "
+                      f"f32 numpy, {cores} threads) of the reference 512/256 grid, extrapolated by padded area "
+                      f"x{area / (side * side):.1f} and {evals_per_iter:.2f} evals/iter"}
 
 
 def run_reference(args):
@@ -293,6 +294,7 @@ def run_reference(args):
     sh, sw = cfgw["style"]
     vals = []
     last = None
+    args.cpu_block = min(args.cpu_block, 512)  # keep the whole reference run to a few minutes
     for i in range(args.warmup + args.steps):
         r = cpu_baseline(args, H, W, sh, sw, args.ref_evals_per_iter)
         if i >= args.warmup:
@@ -317,7 +319,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c4")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--ref-evals-per-iter", type=float, default=1.2)
+    ap.add_argument("--ref-evals-per-iter", type=float, default=2.0)
+    ap.add_argument("--cpu-block", type=int, default=1024, help="CPU sample block side (padded px)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

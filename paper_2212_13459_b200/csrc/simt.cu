@@ -409,7 +409,25 @@ __global__ void __launch_bounds__(kRedThreads) dot3_partial_kernel(const T* a0, 
                                                                    long long n, double* partial) {
   __shared__ double sh[32];
   double s0 = 0, s1 = 0, s2 = 0;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x, nth = (long long)gridDim.x * blockDim.x;
+  long long start = 0;
+  if constexpr (sizeof(T) == 4) {  // float4 body
+    const long long n4 = n / 4;
+    for (long long i = tid; i < n4; i += nth) {
+      const float4 x = reinterpret_cast<const float4*>(a0)[i], y = reinterpret_cast<const float4*>(b0)[i];
+      s0 += (double)x.x * y.x + (double)x.y * y.y + (double)x.z * y.z + (double)x.w * y.w;
+      if (a1) {
+        const float4 u = reinterpret_cast<const float4*>(a1)[i], v = reinterpret_cast<const float4*>(b1)[i];
+        s1 += (double)u.x * v.x + (double)u.y * v.y + (double)u.z * v.z + (double)u.w * v.w;
+      }
+      if (a2) {
+        const float4 u = reinterpret_cast<const float4*>(a2)[i], v = reinterpret_cast<const float4*>(b2)[i];
+        s2 += (double)u.x * v.x + (double)u.y * v.y + (double)u.z * v.z + (double)u.w * v.w;
+      }
+    }
+    start = n4 * 4;
+  }
+  for (long long i = start + tid; i < n; i += nth) {
     s0 += (double)a0[i] * (double)b0[i];
     if (a1) s1 += (double)a1[i] * (double)b1[i];
     if (a2) s2 += (double)a2[i] * (double)b2[i];
@@ -472,7 +490,32 @@ __global__ void __launch_bounds__(kRedThreads) axpy_dot_kernel(AxpyDotArgs a) {
   const T c = v ? (T)(*a.coef) : (T)0;
   const T cs = (T)a.cscale;
   double s = 0.0;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += (long long)gridDim.x * blockDim.x) {
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x, nth = (long long)gridDim.x * blockDim.x;
+  long long start = 0;
+  if constexpr (sizeof(T) == 4) {  // float4 body
+    const long long n4 = a.n / 4;
+    for (long long i = tid; i < n4; i += nth) {
+      float4 q = reinterpret_cast<const float4*>(qi)[i];
+      if (v) {
+        const float4 vv = reinterpret_cast<const float4*>(v)[i];
+        q.x = q.x + c * vv.x;
+        q.y = q.y + c * vv.y;
+        q.z = q.z + c * vv.z;
+        q.w = q.w + c * vv.w;
+      }
+      q.x *= cs;
+      q.y *= cs;
+      q.z *= cs;
+      q.w *= cs;
+      reinterpret_cast<float4*>(qo)[i] = q;
+      if (w) {
+        const float4 ww = reinterpret_cast<const float4*>(w)[i];
+        s += (double)ww.x * q.x + (double)ww.y * q.y + (double)ww.z * q.z + (double)ww.w * q.w;
+      }
+    }
+    start = n4 * 4;
+  }
+  for (long long i = start + tid; i < a.n; i += nth) {
     T q = qi[i];
     if (v) q = q + c * v[i];
     q = q * cs;
@@ -505,8 +548,18 @@ __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(
 // two separate roundings (no FMA contraction), as numpy evaluates x + t * d
 template <typename T>
 __global__ void axpy_kernel(const T* x, const T* d, T t, long long n, T* out) {
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
-    out[i] = add_rn(x[i], mul_rn(t, d[i]));
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x, nth = (long long)gridDim.x * blockDim.x;
+  long long start = 0;
+  if constexpr (sizeof(T) == 4) {
+    const long long n4 = n / 4;
+    for (long long i = tid; i < n4; i += nth) {
+      const float4 a = reinterpret_cast<const float4*>(x)[i], b = reinterpret_cast<const float4*>(d)[i];
+      reinterpret_cast<float4*>(out)[i] = make_float4(add_rn(a.x, mul_rn(t, b.x)), add_rn(a.y, mul_rn(t, b.y)),
+                                                      add_rn(a.z, mul_rn(t, b.z)), add_rn(a.w, mul_rn(t, b.w)));
+    }
+    start = n4 * 4;
+  }
+  for (long long i = start + tid; i < n; i += nth) out[i] = add_rn(x[i], mul_rn(t, d[i]));
 }
 
 // s = xt - x, y = gt - g and partials of <y,s>, <s,s>, <y,y>
@@ -515,7 +568,24 @@ __global__ void __launch_bounds__(kRedThreads) sy_kernel(const T* xt, const T* x
                                                          long long n, T* s, T* y, double* partial) {
   __shared__ double sh[32];
   double ys = 0, ss = 0, yy = 0;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x, nth = (long long)gridDim.x * blockDim.x;
+  long long start = 0;
+  if constexpr (sizeof(T) == 4) {
+    const long long n4 = n / 4;
+    for (long long i = tid; i < n4; i += nth) {
+      const float4 a = reinterpret_cast<const float4*>(xt)[i], b = reinterpret_cast<const float4*>(x)[i];
+      const float4 c = reinterpret_cast<const float4*>(gt)[i], d = reinterpret_cast<const float4*>(g)[i];
+      const float4 si = make_float4(a.x - b.x, a.y - b.y, a.z - b.z, a.w - b.w);
+      const float4 yi = make_float4(c.x - d.x, c.y - d.y, c.z - d.z, c.w - d.w);
+      reinterpret_cast<float4*>(s)[i] = si;
+      reinterpret_cast<float4*>(y)[i] = yi;
+      ys += (double)yi.x * si.x + (double)yi.y * si.y + (double)yi.z * si.z + (double)yi.w * si.w;
+      ss += (double)si.x * si.x + (double)si.y * si.y + (double)si.z * si.z + (double)si.w * si.w;
+      yy += (double)yi.x * yi.x + (double)yi.y * yi.y + (double)yi.z * yi.z + (double)yi.w * yi.w;
+    }
+    start = n4 * 4;
+  }
+  for (long long i = start + tid; i < n; i += nth) {
     const T si = xt[i] - x[i];
     const T yi = gt[i] - g[i];
     s[i] = si;

@@ -269,6 +269,13 @@ def minimize(f, x0, cfg: LBFGSConfig, callback=None, allreduce=None):
     state = LBFGSState()
     d = torch.empty_like(x)
     x_try = torch.empty_like(x)
+    g_spare = torch.empty_like(x) if lazy else None
+    # history ring: m+1 preallocated (s, y) slots; the sy kernel writes the candidate pair into
+    # the spare slot, so a curvature rejection leaves the stored pairs untouched (lbfgs.py:48-59)
+    m = cfg.history_size
+    ring_s = torch.empty((m + 1,) + tuple(x.shape), dtype=x.dtype, device=x.device)
+    ring_y = torch.empty_like(ring_s)
+    slot_of = []  # ring slot of each stored pair, oldest first
     for it in range(cfg.max_iters):
         if gmax <= cfg.grad_tol:
             break
@@ -288,20 +295,30 @@ def minimize(f, x0, cfg: LBFGSConfig, callback=None, allreduce=None):
             t *= cfg.shrink
         if accepted:
             if lazy:
-                g_try = obj.grad(torch.empty_like(x))
+                g_try = obj.grad(g_spare)
                 trace.grads += 1
-            s = torch.empty_like(x)
-            y = torch.empty_like(x)
+            spare = next(k for k in range(m + 1) if k not in slot_of)
+            s, y = ring_s[spare], ring_y[spare]
             ys, ss, yy = vec.sy(x_try, x, g_try, g, s, y)
             if allreduce is not None:
                 tt = torch.tensor([ys, ss, yy], dtype=torch.float64, device=x.device)
                 allreduce(tt)
                 ys, ss, yy = tt.tolist()
-            state.push(s, y, cfg.history_size, dots=(ys, ss, yy))
+            before = len(state.s_hist)
+            if state.push(s, y, m, dots=(ys, ss, yy)):
+                slot_of.append(spare)
+                if len(state.s_hist) == before:  # the oldest pair was evicted
+                    slot_of.pop(0)
             x, x_try = x_try, x
-            loss, g = loss_try, g_try
+            if lazy:
+                g, g_spare = g_try, g
+            else:
+                g = g_try
+            loss = loss_try
         else:
             state.drop_oldest()
+            if slot_of:
+                slot_of.pop(0)
         state.iter = it + 1
         gmax = red_max(g)
         trace.losses.append(loss)

@@ -31,7 +31,7 @@ enum EpiKind : int {
 
 // Parameters of one tcgen05 3x3 implicit-GEMM launch (forward or input-gradient).
 struct ConvArgs {
-  CUtensorMap tm_a_hi, tm_a_lo;  // K operand: input activations (box 8 x 130 x 4 x 2)
+  CUtensorMap tm_r_hi, tm_r_lo;  // K operand: input activations as u64 (2W, H, C_p/8), box 136 x 1 x 1
   CUtensorMap tm_v_hi, tm_v_lo;  // extra-K operand: tap features at the output pixels (box 8 x 128 x 2 x 4)
   const uint8_t* wgt;            // [ntile][kc][pass][tap][kg][n][8] fp16
   const uint8_t* xwgt;           // [ntile][xkc][pass][kg(4)][n][8] fp16 (extra K, 32 ch per chunk)

@@ -33,7 +33,8 @@ namespace spst {
 template <int N>
 struct ConvCfg {
   static constexpr int MT = 2;                      // output rows per tile (M = MT x 128 px)
-  static constexpr int PITCH = 130;                 // 128 output px + 2 halo px
+  static constexpr int PITCH = 136;                 // 128 output px + 2 halo px, padded to 17 x 128 B
+  static constexpr int STRIP = 68;                  // TMA strip (px): two per row at px 0 and 64
   static constexpr int RIN = MT + 2;                // output rows + 2 halo rows
   static constexpr int A_PLANE = RIN * PITCH * 16;  // one 8-channel plane of the window
   static constexpr int A_HALF = 2 * A_PLANE;        // 16 channels
@@ -51,6 +52,7 @@ struct ConvCfg {
   static constexpr int SMEM = STAGES * STAGE + 1024;
   static constexpr int CPG = MT == 2 ? N / 2 : N;   // channels per epilogue warpgroup
   static_assert(2 * XA_HALF <= A_BYTES, "extra-K operand must fit the A area");
+  static_assert(2 * STRIP * 16 == PITCH * 16 && (PITCH * 16) % 128 == 0 && A_PLANE % 128 == 0, "strip layout");
 };
 
 // Chunk schedule of a tile: the n_kc conv chunks, then the n_xkc extra-K (style gradient)
@@ -296,8 +298,8 @@ __global__ void __launch_bounds__(320, 1) conv3x3_tc_kernel(const __grid_constan
   const int n_chunks = a.n_kc + a.n_xkc;
 
   if (warp == 0 && lane == 0) {
-    tma_prefetch_desc(&a.tm_a_hi);
-    tma_prefetch_desc(&a.tm_a_lo);
+    tma_prefetch_desc(&a.tm_r_hi);
+    tma_prefetch_desc(&a.tm_r_lo);
     tma_prefetch_desc(&a.tm_v_hi);
     tma_prefetch_desc(&a.tm_v_lo);
     for (int s = 0; s < C::STAGES; ++s) {
@@ -321,37 +323,46 @@ __global__ void __launch_bounds__(320, 1) conv3x3_tc_kernel(const __grid_constan
 
   if (warp == 0) {
     // ------------------------------------------------------------------ TMA producer
-    if (lane == 0) {
-      uint32_t g = 0;
-      for (int t = first; t < n_tiles; t += step) {
-        const TileId id = decode_tile<CS>(a, t, rank);
-        const int nt = id.nt;
-        const int x0 = id.cx * 128;
-        const int y0 = id.ry * C::MT;
-        for (int c = 0; c < n_chunks; ++c, ++g) {
-          const int s = g % C::STAGES;
-          mbar_wait(&empty_bar[s], ((g / C::STAGES) & 1) ^ 1);
-          uint8_t* st = smem + s * C::STAGE;
-          int ci;
-          const bool extra = chunk_is_extra(c, a.n_kc, ci);
+    // The A window is fetched as 8*RIN strips of 68 pixels (1088 contiguous bytes) -- one per
+    // lane -- through a u64 view of the activation: a box with a 16-byte inner dimension costs
+    // the TMA unit one row per pixel and was measured to throttle the MMA pipe. The two strips
+    // of a row start at px 0 and 64 (128-B aligned smem) and overlap by 4 px.
+    static_assert(8 * C::RIN <= 32, "one A strip per producer lane");
+    const int s_hl = lane / (4 * C::RIN), s_p = (lane / (2 * C::RIN)) & 1, s_r = (lane >> 1) % C::RIN, s_h = lane & 1;
+    const uint32_t s_off = s_hl * C::A_HALF + s_p * C::A_PLANE + (s_r * C::PITCH + s_h * 64) * 16;
+    const void* s_map = s_hl ? (const void*)&a.tm_r_lo : (const void*)&a.tm_r_hi;
+    uint32_t g = 0;
+    for (int t = first; t < n_tiles; t += step) {
+      const TileId id = decode_tile<CS>(a, t, rank);
+      const int nt = id.nt;
+      const int x0 = id.cx * 128;
+      const int y0 = id.ry * C::MT;
+      for (int c = 0; c < n_chunks; ++c, ++g) {
+        const int s = g % C::STAGES;
+        mbar_wait(&empty_bar[s], ((g / C::STAGES) & 1) ^ 1);
+        uint8_t* st = smem + s * C::STAGE;
+        int ci;
+        const bool extra = chunk_is_extra(c, a.n_kc, ci);
 #ifdef SPST_EXP_NOLOAD
-          if (g >= C::STAGES) {
-            mbar_arrive(&full_bar[s]);
-            continue;
-          }
+        if (g >= C::STAGES) {
+          if (lane == 0) mbar_arrive(&full_bar[s]);
+          continue;
+        }
 #endif
+        if (!extra) {
+          if (lane == 0) mbar_arrive_expect_tx(&full_bar[s], C::A_BYTES + C::B_BYTES);
+          __syncwarp();
+          if (lane < 8 * C::RIN)
+            tma_load_3d(st + s_off, s_map, &full_bar[s], 2 * (x0 - 1) + 128 * s_h, y0 - 1 + s_r, 2 * ci + s_p);
+        } else if (lane == 0) {  // extra K (tap features): only the tile's own MT x 128 pixels
+          mbar_arrive_expect_tx(&full_bar[s], 2 * C::XA_HALF + C::XB_BYTES);
+          tma_load_4d(st, &a.tm_v_hi, &full_bar[s], 0, x0, y0, C::XKG * ci);
+          tma_load_4d(st + C::XA_HALF, &a.tm_v_lo, &full_bar[s], 0, x0, y0, C::XKG * ci);
+        }
+        if (lane == 0) {
           const uint8_t* bsrc = extra ? a.xwgt + ((size_t)nt * a.n_xkc + ci) * C::XB_BYTES
                                       : a.wgt + ((size_t)nt * a.n_kc + ci) * C::B_BYTES;
           const uint32_t bbytes = extra ? C::XB_BYTES : C::B_BYTES;
-          if (!extra) {
-            mbar_arrive_expect_tx(&full_bar[s], C::A_BYTES + C::B_BYTES);
-            tma_load_4d(st, &a.tm_a_hi, &full_bar[s], 0, x0 - 1, y0 - 1, 2 * ci);
-            tma_load_4d(st + C::A_HALF, &a.tm_a_lo, &full_bar[s], 0, x0 - 1, y0 - 1, 2 * ci);
-          } else {  // extra K (tap features): only the tile's own MT x 128 pixels
-            mbar_arrive_expect_tx(&full_bar[s], 2 * C::XA_HALF + C::XB_BYTES);
-            tma_load_4d(st, &a.tm_v_hi, &full_bar[s], 0, x0, y0, C::XKG * ci);
-            tma_load_4d(st + C::XA_HALF, &a.tm_v_lo, &full_bar[s], 0, x0, y0, C::XKG * ci);
-          }
           if constexpr (CL) {
             if (rank == 0) bulk_load_multicast(st + C::A_BYTES, bsrc, bbytes, &full_bar[s], kMask);
           } else {

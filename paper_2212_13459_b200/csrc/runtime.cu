@@ -60,6 +60,18 @@ bool map_act(CUtensorMap* m, const __half* base, int n_kg, int H, int W, int mt,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Same activation viewed as u64 (4 fp16) elements: (2W, H, kg); one box is a 68-pixel strip of one
+// 8-channel plane row (1088 contiguous bytes), so TMA moves it as one long row.
+bool map_rows(CUtensorMap* m, const __half* base, int n_kg, int H, int W) {
+  cuuint64_t dims[3] = {2 * (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)n_kg};
+  cuuint64_t strides[2] = {(cuuint64_t)W * 16, (cuuint64_t)H * W * 16};
+  cuuint32_t box[3] = {136, 1, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  return g_encode(m, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, (void*)base, dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // Gram operand: (8 ch, P, kg) view; box (8, 64 px, 16 kg) or, for 64 channels, (8, 256 px, 8 kg)
 bool map_gram(CUtensorMap* m, const __half* base, long long P_range, long long P_total, int n_kg) {
   cuuint64_t dims[3] = {8, (cuuint64_t)P_range, (cuuint64_t)n_kg};
@@ -384,8 +396,8 @@ int run_conv(spst_ctx* ctx, ConvLaunch& L) {
   const HL16* v = L.v ? L.v : in;
   const int N = ntile_for(a.out.C_p);
   const int mt = conv_tc_rows(N);
-  if (!map_act(&a.tm_a_hi, in->hi, in->C_p / 8, in->H, in->W, mt, false) ||
-      !map_act(&a.tm_a_lo, in->lo(), in->C_p / 8, in->H, in->W, mt, false) ||
+  if (!map_rows(&a.tm_r_hi, in->hi, in->C_p / 8, in->H, in->W) ||
+      !map_rows(&a.tm_r_lo, in->lo(), in->C_p / 8, in->H, in->W) ||
       !map_act(&a.tm_v_hi, v->hi, v->C_p / 8, v->H, v->W, mt, true) ||
       !map_act(&a.tm_v_lo, v->lo(), v->C_p / 8, v->H, v->W, mt, true))
     return ctx->fail(SPST_ERR_CUDA, "cuTensorMapEncodeTiled failed");

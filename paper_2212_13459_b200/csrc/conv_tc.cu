@@ -372,8 +372,9 @@ __global__ void __launch_bounds__(320, 1) conv3x3_tc_kernel(const __grid_constan
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
+    // ------------------------------------------------------------------ MMA issuer (whole warp,
+    // one elected lane issues; see umma_f16_ws)
+    {
       const uint32_t idesc = make_idesc_f16(128, N, 0, 0, 0);
       uint32_t g = 0;
       for (int t = first; t < n_tiles; t += step) {
@@ -382,6 +383,7 @@ __global__ void __launch_bounds__(320, 1) conv3x3_tc_kernel(const __grid_constan
           mbar_wait(&cempty_bar[b], ((g / C::NBUF) & 1) ^ 1);
           const int s = g % C::STAGES;
           mbar_wait(&full_bar[s], (g / C::STAGES) & 1);
+          __syncwarp();
           tc_fence_after();
           const uint32_t st = smem_u32(smem + s * C::STAGE);
           const uint32_t bb = st + C::A_BYTES;
@@ -402,7 +404,7 @@ __global__ void __launch_bounds__(320, 1) conv3x3_tc_kernel(const __grid_constan
                 for (int mt = 0; mt < C::MT; ++mt) {
                   const uint64_t ad =
                       adesc0 + (uint64_t)(((pass == 1 ? C::XA_HALF : 0) + mt * 128 * 16 + 2 * ks * C::XA_PLANE) >> 4);
-                  umma_f16(dcol + mt * N, ad, bd, idesc, (pass | ks) ? 1u : 0u);
+                  umma_f16_ws(dcol + mt * N, ad, bd, idesc, (pass | ks) ? 1u : 0u);
                 }
               }
           } else {
@@ -422,16 +424,16 @@ __global__ void __launch_bounds__(320, 1) conv3x3_tc_kernel(const __grid_constan
 #pragma unroll
                 for (int mt = 0; mt < C::MT; ++mt) {
                   const uint64_t ad = ap + (uint64_t)((((mt + dy) * C::PITCH + dx) * 16) >> 4);
-                  umma_f16(dcol + mt * N, ad, bd, idesc, (pass | tap) ? 1u : 0u);  // fresh per chunk
+                  umma_f16_ws(dcol + mt * N, ad, bd, idesc, (pass | tap) ? 1u : 0u);  // fresh per chunk
                 }
               }
             }
           }
           if constexpr (CL)
-            umma_commit_multicast(&empty_bar[s], kMask);  // release the stage in every CTA
+            umma_commit_multicast_ws(&empty_bar[s], kMask);  // release the stage in every CTA
           else
-            umma_commit(&empty_bar[s]);
-          umma_commit(&cfull_bar[b]);
+            umma_commit_ws(&empty_bar[s]);
+          umma_commit_ws(&cfull_bar[b]);
         }
       }
     }

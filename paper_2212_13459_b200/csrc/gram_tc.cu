@@ -76,16 +76,16 @@ __global__ void __launch_bounds__(192, 1) gram_tc_kernel(const __grid_constant__
         uint8_t* st = smem + s * C::STAGE;
         mbar_arrive_expect_tx(&full_bar[s], bytes);
         const int px = (int)(p0 - a.p_begin) + c * C::KPX;  // map base starts at p_begin
-        tma_load_3d(st, &a.tm_hi, &full_bar[s], 0, px, 16 * c1);
-        tma_load_3d(st + C::T_BYTES, &a.tm_lo, &full_bar[s], 0, px, 16 * c1);
+        tma_load_2d(st, &a.tm_hi, &full_bar[s], 2 * px, 16 * c1);  // u64 view: 64 px = 128 elements
+        tma_load_2d(st + C::T_BYTES, &a.tm_lo, &full_bar[s], 2 * px, 16 * c1);
         if (!diag) {
-          tma_load_3d(st + 2 * C::T_BYTES, &a.tm_hi, &full_bar[s], 0, px, 16 * c2);
-          tma_load_3d(st + 3 * C::T_BYTES, &a.tm_lo, &full_bar[s], 0, px, 16 * c2);
+          tma_load_2d(st + 2 * C::T_BYTES, &a.tm_hi, &full_bar[s], 2 * px, 16 * c2);
+          tma_load_2d(st + 3 * C::T_BYTES, &a.tm_lo, &full_bar[s], 2 * px, 16 * c2);
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {  // whole warp, one elected lane issues (umma_f16_ws)
       const uint32_t idesc = make_idesc_f16(128, 128, 0, 1, 1);
       for (int c = 0; c < n_stages; ++c) {
         const int dr = c / C::DRAIN;
@@ -93,6 +93,7 @@ __global__ void __launch_bounds__(192, 1) gram_tc_kernel(const __grid_constant__
         if (c % C::DRAIN == 0) mbar_wait(&cempty_bar[b], ((dr / C::NBUF) & 1) ^ 1);
         const int s = c % C::STAGES;
         mbar_wait(&full_bar[s], (c / C::STAGES) & 1);
+        __syncwarp();
         tc_fence_after();
         const uint32_t st = smem_u32(smem + s * C::STAGE);
         const uint32_t ah = st, al = st + C::T_BYTES;
@@ -106,10 +107,10 @@ __global__ void __launch_bounds__(192, 1) gram_tc_kernel(const __grid_constant__
             const uint32_t off = k * 256;  // 16 px = two 8-px core-matrix groups of 128 B
             const uint64_t da = make_sdesc((pass == 1 ? al : ah) + off, 128, C::KPX * 16);
             const uint64_t db = make_sdesc((pass == 0 ? bl : bh) + off, 128, C::KPX * 16);
-            umma_f16(d, da, db, idesc, (c % C::DRAIN > 0 || pass > 0 || k > 0) ? 1u : 0u);
+            umma_f16_ws(d, da, db, idesc, (c % C::DRAIN > 0 || pass > 0 || k > 0) ? 1u : 0u);
           }
-        umma_commit(&empty_bar[s]);
-        if (c % C::DRAIN == C::DRAIN - 1 || c == n_stages - 1) umma_commit(&cfull_bar[b]);
+        umma_commit_ws(&empty_bar[s]);
+        if (c % C::DRAIN == C::DRAIN - 1 || c == n_stages - 1) umma_commit_ws(&cfull_bar[b]);
       }
     }
   } else {
@@ -150,10 +151,11 @@ __global__ void __launch_bounds__(192, 1) gram_tc_kernel(const __grid_constant__
 // and G = acc1[r] + acc1[64+r] + acc2[r] (lo.lo dropped), i.e. two M128xN64 MMAs per K-step
 // instead of three M128xN128 ones on a half-empty tile.
 struct Gram64Cfg {
-  static constexpr int KPX = 256;                      // pixels per stage
-  static constexpr int PLANE = KPX * 16;               // one 8-channel plane (4 KB)
-  static constexpr int STAGE = 16 * PLANE;             // 8 hi + 8 lo planes (64 KB)
-  static constexpr int STAGES = 3;
+  static constexpr int KPX = 128;                      // pixels per stage (one 2 KB TMA row per plane)
+  static constexpr int PLANE = KPX * 16;               // one 8-channel plane (2 KB)
+  static constexpr int STAGE = 16 * PLANE;             // 8 hi + 8 lo planes (32 KB)
+  static constexpr int STAGES = 6;
+  static constexpr int DRAIN = 2;                      // stages per TMEM accumulator (256 px)
   static constexpr int NBUF = 4;                       // 4 x (acc1 64 + acc2 64) TMEM columns
   static constexpr int SMEM = STAGES * STAGE + 1024;
 };
@@ -196,18 +198,20 @@ __global__ void __launch_bounds__(192, 1) gram64_tc_kernel(const __grid_constant
         uint8_t* st = smem + s * C::STAGE;
         mbar_arrive_expect_tx(&full_bar[s], C::STAGE);
         const int px = (int)(p0 - a.p_begin) + c * C::KPX;
-        tma_load_3d(st, &a.tm_hi, &full_bar[s], 0, px, 0);
-        tma_load_3d(st + 8 * C::PLANE, &a.tm_lo, &full_bar[s], 0, px, 0);
+        tma_load_2d(st, &a.tm_hi, &full_bar[s], 2 * px, 0);  // u64 view: 128 px = 256 elements
+        tma_load_2d(st + 8 * C::PLANE, &a.tm_lo, &full_bar[s], 2 * px, 0);
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {  // whole warp, one elected lane issues (umma_f16_ws)
       const uint32_t idesc = make_idesc_f16(128, 64, 0, 1, 1);
       for (int c = 0; c < n_stages; ++c) {
-        const uint32_t b = c % C::NBUF;
-        mbar_wait(&cempty_bar[b], ((c / C::NBUF) & 1) ^ 1);
+        const int dr = c / C::DRAIN;
+        const uint32_t b = dr % C::NBUF;
+        if (c % C::DRAIN == 0) mbar_wait(&cempty_bar[b], ((dr / C::NBUF) & 1) ^ 1);
         const int s = c % C::STAGES;
         mbar_wait(&full_bar[s], (c / C::STAGES) & 1);
+        __syncwarp();
         tc_fence_after();
         const uint32_t st = smem_u32(smem + s * C::STAGE);
         const uint64_t da0 = make_sdesc(st, 128, C::PLANE);                // [hi;lo] x 16 px
@@ -217,11 +221,12 @@ __global__ void __launch_bounds__(192, 1) gram64_tc_kernel(const __grid_constant
 #pragma unroll 4
         for (int k = 0; k < C::KPX / 16; ++k) {
           const uint64_t off = (uint64_t)((k * 256) >> 4);  // 16 px = two 128-B core-matrix groups
-          umma_f16(d2, da0 + off, dl0 + off, idesc, k > 0 ? 1u : 0u);  // small (x lo) first
-          umma_f16(d1, da0 + off, dh0 + off, idesc, k > 0 ? 1u : 0u);
+          const uint32_t acc = (c % C::DRAIN > 0 || k > 0) ? 1u : 0u;
+          umma_f16_ws(d2, da0 + off, dl0 + off, idesc, acc);  // small (x lo) first
+          umma_f16_ws(d1, da0 + off, dh0 + off, idesc, acc);
         }
-        umma_commit(&empty_bar[s]);
-        umma_commit(&cfull_bar[b]);
+        umma_commit_ws(&empty_bar[s]);
+        if (c % C::DRAIN == C::DRAIN - 1 || c == n_stages - 1) umma_commit_ws(&cfull_bar[b]);
       }
     }
   } else {
@@ -230,7 +235,8 @@ __global__ void __launch_bounds__(192, 1) gram64_tc_kernel(const __grid_constant
     float acc[64];
 #pragma unroll
     for (int i = 0; i < 64; ++i) acc[i] = 0.f;
-    for (int c = 0; c < n_stages; ++c) {
+    const int n_drains = (n_stages + C::DRAIN - 1) / C::DRAIN;
+    for (int c = 0; c < n_drains; ++c) {
       const uint32_t b = c % C::NBUF;
       mbar_wait(&cfull_bar[b], (c / C::NBUF) & 1);
       tc_fence_after();

@@ -72,14 +72,16 @@ bool map_rows(CUtensorMap* m, const __half* base, int n_kg, int H, int W) {
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// Gram operand: (8 ch, P, kg) view; box (8, 64 px, 16 kg) or, for 64 channels, (8, 256 px, 8 kg)
+// Gram operand: the HL16 planes viewed as u64 (2P, kg); box (128 = 64 px, 16 kg) or, for 64
+// channels, (256 = 128 px, 8 kg).  Each box row is one plane's contiguous pixel run (1-2 KB),
+// landing as the dense [kg][px][8] MN-major operand.
 bool map_gram(CUtensorMap* m, const __half* base, long long P_range, long long P_total, int n_kg) {
-  cuuint64_t dims[3] = {8, (cuuint64_t)P_range, (cuuint64_t)n_kg};
-  cuuint64_t strides[2] = {16, (cuuint64_t)P_total * 16};
+  cuuint64_t dims[2] = {2 * (cuuint64_t)P_range, (cuuint64_t)n_kg};
+  cuuint64_t strides[1] = {(cuuint64_t)P_total * 16};
   const bool c64 = n_kg == 8;
-  cuuint32_t box[3] = {8, c64 ? 256u : 64u, c64 ? 8u : 16u};
-  cuuint32_t es[3] = {1, 1, 1};
-  return g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, (void*)base, dims, strides, box, es,
+  cuuint32_t box[2] = {c64 ? 256u : 128u, c64 ? 8u : 16u};
+  cuuint32_t es[2] = {1, 1};
+  return g_encode(m, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, (void*)base, dims, strides, box, es,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }

@@ -70,21 +70,17 @@ struct GramArgs {
 
 constexpr int kFirstC = 64;  // first-layer output channels supported by the SIMT kernels (padded)
 
-struct FirstConvArgs {
+// Preprocessed, replicate-padded image as the first conv's K operand: one 8-channel HL16 plane
+// (3 channels + 5 zeros); the conv's second 8-channel K group reads out of bounds (TMA zero fill).
+struct ImageHLArgs {
   const float* img;   // (h, w, 3) f32, unpadded global image
   int h, w;           // unpadded global dims
   int row_off;        // global padded row of local row 0
   int Hl, Wp;         // local grid (rows) x padded width
   int perm[3];
   float mean[3], scale[3];
-  float wgt[kFirstC * 27];  // [C_out][3][3][3] f32, zero padded (kernel-parameter constant bank)
-  float bias[kFirstC];
-  int C_out, C_out_p;
-  HL16 out;
-  uint32_t* mask;
-  float* colsum_partial;  // [blocks][C_out_p] nullable
-  int sum_r0, sum_r1;     // local rows contributing to sums
-  unsigned int* amax;
+  HL16 out;           // C_p = 8
+  unsigned int* amax; // max |preprocessed value| (float bits)
 };
 
 struct FirstConvBwdArgs {
@@ -140,8 +136,7 @@ cudaError_t launch_gram64_tc(const GramArgs& a, int n_splits, int C, double inv_
                              cudaStream_t stream);
 cudaError_t launch_gram_reduce(const float* partial, int n_splits, int n_ctile, int C, double inv_scale2,
                                double* S, cudaStream_t stream);
-cudaError_t launch_first_conv_fwd(const FirstConvArgs& a, cudaStream_t st);
-int first_conv_fwd_blocks(int Hl, int Wp);
+cudaError_t launch_image_hl(const ImageHLArgs& a, cudaStream_t st);
 cudaError_t launch_first_conv_bwd(const FirstConvBwdArgs& a, cudaStream_t st);
 cudaError_t launch_fold_grad(const float* gimg, int Hl, int Wp, int row_off, int h, int w, int r0, int r1,
                              float* grad, cudaStream_t st);

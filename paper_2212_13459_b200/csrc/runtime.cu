@@ -146,7 +146,6 @@ struct Stage {
   std::vector<double> w, b;
   int wexp = 0;
   float* bias_d = nullptr;
-  float* w1_d = nullptr;
   uint8_t* wf_d = nullptr;
   uint8_t* wb_d = nullptr;
   int H = 0, W = 0;
@@ -175,7 +174,9 @@ struct spst_ctx {
   long long alloc_bytes = 0;
   bool bound = false;
   int h = 0, w = 0, Hp = 0, Wp = 0, grid_r0 = 0, grid_r1 = 0, own_r0 = 0, own_r1 = 0;
-  unsigned int* amax_d = nullptr;  // [stages][4]: out, pooled, grad, addend
+  unsigned int* amax_d = nullptr;  // [stages][4]: out, pooled, grad, addend; [4 * stages]: image
+  HL16 img;                        // first conv's K operand (8-channel HL16 image), see image_hl_kernel
+  Expo img_e;
   std::vector<unsigned int> amax_h;
   HL16 gbuf[2];
   size_t gbuf_elems = 0;
@@ -294,7 +295,7 @@ int parse_net(spst_ctx* ctx, int n_layers, const int* kinds, const int* cin, con
     if (s.cin != prev_c) return ctx->fail(SPST_ERR_SHAPE, "conv input channels do not chain");
     if (ctx->stages.empty() && s.cout > kFirstC)
       return ctx->fail(SPST_ERR_UNSUPPORTED, "first conv layer supports at most 64 output channels");
-    s.cin_p = ctx->stages.empty() ? 3 : round_up(s.cin, 64);
+    s.cin_p = ctx->stages.empty() ? 16 : round_up(s.cin, 64);  // image: one 16-channel K chunk
     s.cout_p = round_up(s.cout, 64);
     s.stride = stride;
     s.w.assign(weights[i], weights[i] + (size_t)s.cout * s.cin * 9);
@@ -348,18 +349,11 @@ int upload_weights(spst_ctx* ctx) {
     s.bias_d = ctx->dalloc<float>(s.cout_p, true);
     if (!s.bias_d) return ctx->fail(SPST_ERR_OOM, "bias upload");
     CK(cudaMemcpy(s.bias_d, b32.data(), b32.size() * 4, cudaMemcpyHostToDevice));
-    if (k == 0) {
-      std::vector<float> w32(s.w.size());
-      for (size_t j = 0; j < w32.size(); ++j) w32[j] = (float)s.w[j];
-      s.w1_d = ctx->dalloc<float>(w32.size(), true);
-      if (!s.w1_d) return ctx->fail(SPST_ERR_OOM, "first-layer weights");
-      CK(cudaMemcpy(s.w1_d, w32.data(), w32.size() * 4, cudaMemcpyHostToDevice));
-    }
-    if (k > 0) {
-      auto wf = stage_slabs(s, false, ntile_for(s.cout_p));
-      s.wf_d = ctx->dalloc<uint8_t>(wf.size() * 2, true);
-      if (!s.wf_d) return ctx->fail(SPST_ERR_OOM, "forward weight slabs");
-      CK(cudaMemcpy(s.wf_d, wf.data(), wf.size() * 2, cudaMemcpyHostToDevice));
+    auto wf = stage_slabs(s, false, ntile_for(s.cout_p));
+    s.wf_d = ctx->dalloc<uint8_t>(wf.size() * 2, true);
+    if (!s.wf_d) return ctx->fail(SPST_ERR_OOM, "forward weight slabs");
+    CK(cudaMemcpy(s.wf_d, wf.data(), wf.size() * 2, cudaMemcpyHostToDevice));
+    if (k > 0) {  // the first conv's adjoint runs on CUDA cores (first_conv_bwd_kernel)
       auto wb = stage_slabs(s, true, ntile_for(s.cin_p));
       s.wb_d = ctx->dalloc<uint8_t>(wb.size() * 2, true);
       if (!s.wb_d) return ctx->fail(SPST_ERR_OOM, "backward weight slabs");
@@ -404,7 +398,7 @@ int run_conv(spst_ctx* ctx, ConvLaunch& L) {
       !map_act(&a.tm_v_lo, v->lo(), v->C_p / 8, v->H, v->W, mt, true))
     return ctx->fail(SPST_ERR_CUDA, "cuTensorMapEncodeTiled failed");
   a.wgt = L.in ? L.wslab : nullptr;
-  a.n_kc = L.in ? L.in->C_p / 16 : 0;
+  a.n_kc = L.in ? (L.in->C_p + 15) / 16 : 0;  // an 8-channel input reads its 2nd K group as TMA zero fill
   a.xwgt = reinterpret_cast<const uint8_t*>(L.xw);
   a.n_xkc = L.xw ? v->C_p / (8 * conv_tc_xkg(N)) : 0;
   a.H = L.H;
@@ -445,34 +439,25 @@ int forward_stage(spst_ctx* ctx, int k, const float* x) {
   s.pooled.scale = pow2f(s.pool_e.e);
   CK(cudaMemsetAsync(ctx->amax_d + 4 * k, 0, 8, ctx->stream));
   if (k == 0) {
-    FirstConvArgs a{};
-    a.img = x;
-    a.h = ctx->h;
-    a.w = ctx->w;
-    a.row_off = ctx->grid_r0;
-    a.Hl = s.H;
-    a.Wp = s.W;
+    ImageHLArgs ia{};
+    ia.img = x;
+    ia.h = ctx->h;
+    ia.w = ctx->w;
+    ia.row_off = ctx->grid_r0;
+    ia.Hl = s.H;
+    ia.Wp = s.W;
     for (int c = 0; c < 3; ++c) {
-      a.perm[c] = ctx->perm[c];
-      a.mean[c] = ctx->mean[c];
-      a.scale[c] = ctx->scale[c];
+      ia.perm[c] = ctx->perm[c];
+      ia.mean[c] = ctx->mean[c];
+      ia.scale[c] = ctx->scale[c];
     }
-    for (int i = 0; i < kFirstC * 27; ++i) a.wgt[i] = i < (int)s.w.size() ? (float)s.w[i] : 0.f;
-    for (int i = 0; i < kFirstC; ++i) a.bias[i] = i < s.cout ? (float)s.b[i] : 0.f;
-    a.C_out = s.cout;
-    a.C_out_p = s.cout_p;
-    a.out = s.out;
-    a.mask = s.mask;
-    a.colsum_partial = tap ? tap->colsum_partial : nullptr;
-    a.sum_r0 = own0;
-    a.sum_r1 = own1;
-    a.amax = ctx->amax_d + 4 * k;
-    CK(launch_first_conv_fwd(a, ctx->stream));
-    if (s.pool_after) CK(launch_pool2_hl(s.out, s.pooled, ctx->amax_d + 4 * k + 1, ctx->stream));
-    return SPST_OK;
+    ctx->img.scale = pow2f(ctx->img_e.e);
+    ia.out = ctx->img;
+    ia.amax = ctx->amax_d + 4 * ctx->stages.size();
+    CK(cudaMemsetAsync(ia.amax, 0, 4, ctx->stream));
+    CK(launch_image_hl(ia, ctx->stream));
   }
-  const Stage& p = ctx->stages[k - 1];
-  const HL16& in = p.pool_after ? p.pooled : p.out;
+  const HL16& in = k == 0 ? ctx->img : (ctx->stages[k - 1].pool_after ? ctx->stages[k - 1].pooled : ctx->stages[k - 1].out);
   ConvLaunch L;
   L.in = &in;
   L.wslab = s.wf_d;
@@ -533,22 +518,33 @@ int do_forward(spst_ctx* ctx, const float* x, bool careful) {
   const int n = (int)ctx->stages.size();
   for (int k = 0; k < n; ++k) {
     Stage& s = ctx->stages[k];
-    const bool check = careful || !s.out_e.known || (s.pool_after && !s.pool_e.known);
+    const bool check = careful || !s.out_e.known || (s.pool_after && !s.pool_e.known) || (k == 0 && !ctx->img_e.known);
     for (int attempt = 0; attempt < 6; ++attempt) {
       TRY(forward_stage(ctx, k, x));
       if (!check) break;
+      bool img_ok = true;
+      if (k == 0) {  // the image operand is range-checked like every stored tensor
+        const float mi = read_amax(ctx, 4 * n);
+        img_ok = !range_bad(mi, ctx->img.scale);
+        ctx->img_e = {choose_exp(mi), true};
+      }
       const float m0 = read_amax(ctx, 4 * k), m1 = read_amax(ctx, 4 * k + 1);
-      const bool ok = stage_ranges_ok(ctx, k, m0, m1);
+      const bool ok = stage_ranges_ok(ctx, k, m0, m1) && img_ok;
       if (s.has_out) s.out_e = {choose_exp(m0), true};
       if (s.pool_after) s.pool_e = {choose_exp(m1), true};
       if (ok) break;
     }
   }
   for (int k = 0; k < n; ++k) TRY(stage_stats(ctx, k));
-  ctx->amax_h.resize(4 * n);
-  CK(cudaMemcpyAsync(ctx->amax_h.data(), ctx->amax_d, 16 * n, cudaMemcpyDeviceToHost, ctx->stream));
+  ctx->amax_h.resize(4 * n + 4);
+  CK(cudaMemcpyAsync(ctx->amax_h.data(), ctx->amax_d, 16 * n + 16, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   bool bad = false;
+  {
+    const float mi = bits_to_float(ctx->amax_h[4 * n]);
+    if (!std::isfinite(mi) || mi * ctx->img.scale > kOverflow) bad = true;
+    if (mi > 0 && std::isfinite(mi)) ctx->img_e = {choose_exp(mi), true};
+  }
   for (int k = 0; k < n; ++k) {
     Stage& s = ctx->stages[k];
     const float m0 = bits_to_float(ctx->amax_h[4 * k]), m1 = bits_to_float(ctx->amax_h[4 * k + 1]);
@@ -757,10 +753,15 @@ int do_backward(spst_ctx* ctx, double two_lambda, float* grad, bool careful) {
   const int r0 = ctx->own_r0, r1 = std::min(ctx->own_r1, ctx->h);
   CK(launch_fold_grad(ctx->gimg, s0.H, s0.W, ctx->grid_r0, ctx->h, ctx->w, r0, r1, grad, ctx->stream));
   // end-of-pass range check (fast path)
-  ctx->amax_h.resize(4 * n);
-  CK(cudaMemcpyAsync(ctx->amax_h.data(), ctx->amax_d, 16 * n, cudaMemcpyDeviceToHost, ctx->stream));
+  ctx->amax_h.resize(4 * n + 4);
+  CK(cudaMemcpyAsync(ctx->amax_h.data(), ctx->amax_d, 16 * n + 16, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   bool bad = false;
+  {
+    const float mi = bits_to_float(ctx->amax_h[4 * n]);
+    if (!std::isfinite(mi) || mi * ctx->img.scale > kOverflow) bad = true;
+    if (mi > 0 && std::isfinite(mi)) ctx->img_e = {choose_exp(mi), true};
+  }
   for (int k = 0; k < n; ++k) {
     Stage& s = ctx->stages[k];
     const float m = bits_to_float(ctx->amax_h[4 * k + 2]);
@@ -780,8 +781,8 @@ int bind_alloc(spst_ctx* ctx) {
     s.H = Hl / s.stride;
     s.W = ctx->Wp / s.stride;
     const bool tap = s.style >= 0 || s.content;
-    s.has_out = (k == 0) || !s.pool_after || tap;
-    s.store_out = s.pool_after && tap && k > 0;
+    s.has_out = !s.pool_after || tap;
+    s.store_out = s.pool_after && tap;
     s.out = hl_shape(s.cout_p, s.H, s.W);
     if (s.has_out) {
       s.out.hi = ctx->dalloc<__half>((size_t)s.cout_p * s.H * s.W * 2);
@@ -818,7 +819,7 @@ int bind_alloc(spst_ctx* ctx) {
       t.gram_splits = (int)std::max<long long>(1, (own_px + t.gram_px - 1) / t.gram_px);
       t.gram_partial = ctx->dalloc<float>((size_t)t.gram_splits * (nct * (nct + 1) / 2) * 128 * 128);
       const int mt = conv_tc_rows(ntile_for(s.cout_p));
-      t.colsum_rows = k == 0 ? first_conv_fwd_blocks(s.H, s.W) : ((s.W + 127) / 128) * ((s.H + mt - 1) / mt) * 2 * mt;
+      t.colsum_rows = ((s.W + 127) / 128) * ((s.H + mt - 1) / mt) * 2 * mt;
       t.colsum_partial = ctx->dalloc<float>((size_t)t.colsum_rows * Cp);
       t.colsum_mid = ctx->dalloc<double>((size_t)kColsumMid * Cp);
       if (!t.S || !t.s || !t.mu || !t.sd || !t.ratio || !t.row_loss || !t.row_mmax || !t.ms_loss || !t.degenerate ||
@@ -847,13 +848,16 @@ int bind_alloc(spst_ctx* ctx) {
   ctx->addend.hi = ctx->dalloc<__half>(std::max<size_t>(admax, 16));
   ctx->addend_elems = admax;
   ctx->gimg = ctx->dalloc<float>((size_t)Hl * ctx->Wp * 3);
-  ctx->amax_d = ctx->dalloc<unsigned int>(4 * n);
+  ctx->amax_d = ctx->dalloc<unsigned int>(4 * n + 4);
+  ctx->img = hl_shape(8, Hl, ctx->Wp);
+  ctx->img.hi = ctx->dalloc<__half>((size_t)8 * Hl * ctx->Wp * 2);
+  if (!ctx->img.hi) return ctx->fail(SPST_ERR_OOM, "image operand");
   ctx->content_partial = ctx->dalloc<double>(red_blocks() + 8);
   ctx->zero_xw = ctx->dalloc<__half>((size_t)max_cp * max_cp * 2);
   if (!ctx->addend.hi || !ctx->gimg || !ctx->amax_d || !ctx->content_partial || !ctx->zero_xw)
     return ctx->fail(SPST_ERR_OOM, "workspace");
   CK(cudaMemset(ctx->zero_xw, 0, (size_t)max_cp * max_cp * 2 * sizeof(__half)));
-  CK(cudaMemset(ctx->amax_d, 0, 16 * n));
+  CK(cudaMemset(ctx->amax_d, 0, 16 * n + 16));
   if (ctx->content_stage >= 0) {
     const Stage& s = ctx->stages[ctx->content_stage];
     ctx->content_u = hl_shape(s.cout_p, s.H, s.W);

@@ -8,6 +8,8 @@
 //     117-165), content squared distance (localized.py:257-267)
 //   * deterministic f64 reductions, L-BFGS vector passes (lbfgs.py:68-142)
 //   * area downsampling and half-pixel bilinear resampling (tensorops.py:136-185)
+#include <algorithm>
+
 #include "common.cuh"
 #include "sm100.cuh"
 
@@ -19,101 +21,33 @@ namespace spst {
 
 constexpr int FC_BX = 32, FC_BY = 8;
 
-__device__ __forceinline__ float warp_transpose_sum32(float (&v)[32]) {
-  const uint32_t lane = threadIdx.x & 31;
+// Image -> first-conv operand (reference extractor.py preprocessing + the replicate padding of
+// localized.py): v_c = (img[perm c] - mean_c) / scale_c at the clamped global pixel, split into
+// fp16 hi/lo at scale out.scale.  One thread per grid pixel, 16 B hi + 16 B lo per pixel.
+__global__ void __launch_bounds__(256) image_hl_kernel(const __grid_constant__ ImageHLArgs a) {
+  const long long n = (long long)a.Hl * a.Wp;
+  float m = 0.f;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const int y = (int)(i / a.Wp), x = (int)(i % a.Wp);
+    const int gy = min(y + a.row_off, a.h - 1), gx = min(x, a.w - 1);
+    const float* px = a.img + ((size_t)gy * a.w + gx) * 3;
+    __align__(16) __half hh[8];
+    __align__(16) __half ll[8];
 #pragma unroll
-  for (int off = 16; off >= 1; off >>= 1) {
-#pragma unroll
-    for (int i = 0; i < off; ++i) {
-      float send = (lane & off) ? v[i] : v[i + off];
-      float keep = (lane & off) ? v[i + off] : v[i];
-      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+    for (int c = 0; c < 8; ++c) {
+      float v = 0.f;
+      if (c < 3) v = (px[a.perm[c]] - a.mean[c]) / a.scale[c];
+      m = fmaxf(m, fabsf(v));
+      HalfPair p = split_f16(v * a.out.scale);
+      hh[c] = p.hi;
+      ll[c] = p.lo;
     }
+    reinterpret_cast<uint4*>(a.out.hi)[i] = *reinterpret_cast<uint4*>(hh);
+    reinterpret_cast<uint4*>(a.out.lo())[i] = *reinterpret_cast<uint4*>(ll);
   }
-  return v[0];
-}
-
-// Weights and bias come from the kernel-parameter constant bank with compile-time indices, so
-// every FFMA takes its weight operand straight from the constant cache.
-__global__ void __launch_bounds__(256) first_conv_fwd_kernel(const __grid_constant__ FirstConvArgs a) {
-  __shared__ float tile[3][FC_BY + 2][FC_BX + 2];
-  __shared__ float csum[FC_BY][32];
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  const int x0 = blockIdx.x * FC_BX, y0 = blockIdx.y * FC_BY;
-  for (int i = threadIdx.x; i < 3 * (FC_BY + 2) * (FC_BX + 2); i += blockDim.x) {
-    const int c = i / ((FC_BY + 2) * (FC_BX + 2));
-    const int r = (i / (FC_BX + 2)) % (FC_BY + 2);
-    const int cc = i % (FC_BX + 2);
-    const int yl = y0 - 1 + r, xl = x0 - 1 + cc;
-    float v = 0.f;
-    if (yl >= 0 && yl < a.Hl && xl >= 0 && xl < a.Wp) {
-      const int gy = min(yl + a.row_off, a.h - 1), gx = min(xl, a.w - 1);
-      v = (a.img[((size_t)gy * a.w + gx) * 3 + a.perm[c]] - a.mean[c]) / a.scale[c];
-    }
-    tile[c][r][cc] = v;
-  }
-  __syncthreads();
-  float in[27];
 #pragma unroll
-  for (int c = 0; c < 3; ++c)
-#pragma unroll
-    for (int dy = 0; dy < 3; ++dy)
-#pragma unroll
-      for (int dx = 0; dx < 3; ++dx) in[c * 9 + dy * 3 + dx] = tile[c][ty + dy][tx + dx];
-  const int y = y0 + ty, x = x0 + tx;
-  const bool ok = y < a.Hl && x < a.Wp;
-  const bool in_sum = ok && y >= a.sum_r0 && y < a.sum_r1;
-  float amax = 0.f;
-#pragma unroll
-  for (int cg = 0; cg < kFirstC; cg += 32) {
-    float v[32];
-    uint32_t bits = 0;
-#pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      float acc = a.bias[cg + j];
-#pragma unroll
-      for (int i = 0; i < 27; ++i) acc = fmaf(in[i], a.wgt[(cg + j) * 27 + i], acc);
-      bits |= (acc > 0.f ? 1u : 0u) << j;
-      v[j] = fmaxf(acc, 0.f);
-      amax = fmaxf(amax, ok ? v[j] : 0.f);
-    }
-    if (cg >= a.C_out_p) break;
-    if (ok) {
-      a.mask[((size_t)(cg >> 5) * a.Hl + y) * a.Wp + x] = bits;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        __align__(16) __half hh[8];
-        __align__(16) __half ll[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          HalfPair p = split_f16(v[8 * k + e] * a.out.scale);
-          hh[e] = p.hi;
-          ll[e] = p.lo;
-        }
-        const size_t off = ((size_t)((cg >> 3) + k) * a.out.H + y) * a.out.W + x;
-        reinterpret_cast<uint4*>(a.out.hi)[off] = *reinterpret_cast<uint4*>(hh);
-        reinterpret_cast<uint4*>(a.out.lo())[off] = *reinterpret_cast<uint4*>(ll);
-      }
-    }
-    if (a.colsum_partial) {
-#pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] = in_sum ? v[j] : 0.f;
-      csum[ty][tx] = warp_transpose_sum32(v);
-      __syncthreads();
-      if (ty == 0) {
-        float s = 0.f;
-        for (int r = 0; r < FC_BY; ++r) s += csum[r][tx];
-        const size_t blk = (size_t)blockIdx.y * gridDim.x + blockIdx.x;
-        a.colsum_partial[blk * a.C_out_p + cg + tx] = s;
-      }
-      __syncthreads();
-    }
-  }
-  if (a.amax) {
-#pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, off));
-    if (tx == 0 && amax > 0.f) atomicMax(a.amax, __float_as_uint(amax));
-  }
+  for (int off = 16; off >= 1; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+  if ((threadIdx.x & 31) == 0 && m > 0.f) atomicMax(a.amax, __float_as_uint(m));
 }
 
 __global__ void __launch_bounds__(256) first_conv_bwd_kernel(const __grid_constant__ FirstConvBwdArgs a) {
@@ -656,12 +590,12 @@ __global__ void resize_bilinear_kernel(const float* in, int h, int w, int c, int
 // ------------------------------------------------------------------------------------------
 // launch helpers
 // ------------------------------------------------------------------------------------------
-cudaError_t launch_first_conv_fwd(const FirstConvArgs& a, cudaStream_t st) {
-  dim3 grid((a.Wp + FC_BX - 1) / FC_BX, (a.Hl + FC_BY - 1) / FC_BY);
-  first_conv_fwd_kernel<<<grid, 256, 0, st>>>(a);
+cudaError_t launch_image_hl(const ImageHLArgs& a, cudaStream_t st) {
+  const long long n = (long long)a.Hl * a.Wp;
+  const int blocks = (int)std::min<long long>((n + 255) / 256, 148LL * 8);
+  image_hl_kernel<<<blocks, 256, 0, st>>>(a);
   return cudaGetLastError();
 }
-int first_conv_fwd_blocks(int Hl, int Wp) { return ((Wp + FC_BX - 1) / FC_BX) * ((Hl + FC_BY - 1) / FC_BY); }
 
 cudaError_t launch_first_conv_bwd(const FirstConvBwdArgs& a, cudaStream_t st) {
   dim3 grid((a.g.W + FC_BX - 1) / FC_BX, (a.g.H + FC_BY - 1) / FC_BY);

@@ -11,6 +11,8 @@
  *   lbfgs.py:99       minimize          -> spst_vec_axpy / spst_vec_sy / spst_vec_absmax
  *   tensorops.py:136  resize_down       -> spst_resize_down
  *   tensorops.py:158  resize_bilinear   -> spst_resize_bilinear
+ *   metrics.py:24     psnr              -> spst_metric_sqdiff
+ *   metrics.py:55     ssim              -> spst_metric_ssim
  * The reference has no FFI for this path (it is pure NumPy); the Python package
  * paper_2212_13459_b200 binds these symbols with ctypes.
  *
@@ -118,6 +120,19 @@ int spst_vec_axpy(int f64, const void* x, const void* d, double t, long long n, 
 int spst_vec_sy(int f64, const void* xt, const void* x, const void* gt, const void* g, long long n,
                 void* s, void* y, double* partial_dev, double* out_dev /*[3]: ys, ss, yy*/,
                 void* stream);
+
+/* ---------------------------------------------------------------- metrics --------------- *
+ * metrics.py:24-31 psnr: out_dev[0] = sum over n elements of (a-b)^2 (f64, fixed order).
+ * metrics.py:55-73 ssim: out_dev[0] = sum of the SSIM map of the Rec.601 luma of two (h, w, c)
+ *   images (c = 1 or 3), 11x11 Gaussian window sigma 1.5, valid mode, K1/K2 = 0.01/0.03; the
+ *   caller divides by (h-10)(w-10).  h, w >= 11 else SPST_ERR_SHAPE.
+ * partial_dev holds spst_vec_partials() doubles.  sqdiff: f64 selects float64 for both inputs;
+ * ssim: f64 is a mask (bit 0: a is float64, bit 1: b is float64), each luma is formed in its
+ * image's own dtype as the reference's NumPy code does. */
+int spst_metric_sqdiff(int f64, const void* a, const void* b, long long n, double* partial_dev,
+                       double* out_dev, void* stream);
+int spst_metric_ssim(int f64, const void* a, const void* b, int h, int w, int c, double* partial_dev,
+                     double* out_dev, void* stream);
 
 /* ---------------------------------------------------------------- resampling ------------ */
 int spst_resize_down(const float* in, int h, int w, int c, int factor, float* out, void* stream);

@@ -641,3 +641,44 @@ def lambda_for_scale(net, dims, lam=1.0):
     s_, _, c = net.geometry(net.content_tap)
     ph, pw = padded_dims(net, *dims)
     return lam / (c * (ph // s_) * (pw // s_))
+
+
+# ----------------------------------------------------------------------------------------
+# evaluation metrics (metrics.py:17-73)
+# ----------------------------------------------------------------------------------------
+def psnr(a, b):
+    """metrics.py:24-31: 10 log10(1 / mean((a-b)^2)) in f64, +inf when identical."""
+    err = np.asarray(a, dtype=np.float64) - np.asarray(b, dtype=np.float64)
+    mse = float(np.mean(err * err))
+    return math.inf if mse == 0.0 else -10.0 * math.log10(mse)
+
+
+def luma(img):
+    """metrics.py:34-38 (Rec. 601).  The weights are Python floats, so an f32 image is weighted
+    in f32 (NumPy weak-scalar promotion) and only then widened."""
+    img = np.asarray(img)
+    if img.ndim == 2:
+        return img.astype(np.float64)
+    dt = img.dtype.type if img.dtype in (np.float32, np.float64) else np.float64
+    w = [dt(c) for c in (0.299, 0.587, 0.114)]
+    x = img.astype(dt, copy=False)
+    return ((w[0] * x[..., 0] + w[1] * x[..., 1]) + w[2] * x[..., 2]).astype(np.float64)
+
+
+def ssim(a, b, win=11, sigma=1.5, k1=0.01, k2=0.03):
+    """metrics.py:41-73: mean SSIM map of the luma, separable Gaussian window in valid mode."""
+    t = np.arange(win, dtype=np.float64) - (win - 1) / 2.0
+    g = np.exp(-t * t / (2.0 * sigma * sigma))
+    g /= g.sum()
+
+    def blur(f):  # valid-mode separable filter, rows then columns
+        h, w = f.shape
+        rows = sum(g[j] * f[j:h - win + 1 + j, :] for j in range(win))
+        return sum(g[j] * rows[:, j:w - win + 1 + j] for j in range(win))
+
+    x, y = luma(a), luma(b)
+    mx, my = blur(x), blur(y)
+    vx, vy, cxy = blur(x * x) - mx * mx, blur(y * y) - my * my, blur(x * y) - mx * my
+    c1, c2 = k1 * k1, k2 * k2
+    smap = ((2 * mx * my + c1) * (2 * cxy + c2)) / ((mx * mx + my * my + c1) * (vx + vy + c2))
+    return float(smap.mean())

@@ -12,6 +12,7 @@ from .errors import (ConfigError, DegenerateStdWarning, EmptyError, FormatError,
 from .lbfgs import LBFGSConfig, LBFGSState, Trace, minimize, two_loop_direction
 from .localized import (TransferProblem, build_problem, loss_grad, loss_grad_global, make_grid, stats_pass,
                         track_activations)
+from .metrics import IdentityReport, append_csv, gram_distance, identity_test, psnr, ssim
 from .pipeline import (RunConfig, Schedule, make_schedule, multiscale_transfer, scale_dims,
                        synthesis_scales_for, texture_synthesize)
 from .resample import resize_bilinear, resize_down, resize_up2

@@ -162,5 +162,10 @@ cudaError_t launch_resize_down(const float* in, int h, int w, int c, int f, floa
 cudaError_t launch_resize_bilinear(const float* in, int h, int w, int c, int oh, int ow, float* out,
                                    cudaStream_t st);
 int red_blocks();
+// metrics.cu (reference metrics.py): partial holds red_blocks() doubles; out = fixed-order sum
+cudaError_t launch_metric_sqdiff(bool f64, const void* a, const void* b, long long n, double* partial, double* out,
+                                 cudaStream_t st);
+cudaError_t launch_metric_ssim(int f64_mask, const void* a, const void* b, int h, int w, int c, double* partial,
+                               double* out, cudaStream_t st);
 
 }  // namespace spst

@@ -1154,6 +1154,21 @@ int spst_vec_sum_partials(const double* partial, int nk, double* out, void* stre
   return launch_sum_partials(partial, nk, out, (cudaStream_t)stream) == cudaSuccess ? SPST_OK : SPST_ERR_CUDA;
 }
 
+int spst_metric_sqdiff(int f64, const void* a, const void* b, long long n, double* partial, double* out,
+                       void* stream) {
+  if (n < 0 || !a || !b || !partial || !out) return SPST_ERR_SHAPE;
+  return launch_metric_sqdiff(f64 != 0, a, b, n, partial, out, (cudaStream_t)stream) == cudaSuccess ? SPST_OK
+                                                                                                  : SPST_ERR_CUDA;
+}
+
+int spst_metric_ssim(int f64, const void* a, const void* b, int h, int w, int c, double* partial, double* out,
+                     void* stream) {
+  if (h < 11 || w < 11 || (c != 1 && c != 3) || !a || !b || !partial || !out) return SPST_ERR_SHAPE;
+  return launch_metric_ssim(f64, a, b, h, w, c, partial, out, (cudaStream_t)stream) == cudaSuccess
+             ? SPST_OK
+             : SPST_ERR_CUDA;
+}
+
 int spst_vec_axpy(int f64, const void* x, const void* d, double t, long long n, void* out, void* stream) {
   return launch_axpy(f64, x, d, t, n, out, (cudaStream_t)stream) == cudaSuccess ? SPST_OK : SPST_ERR_CUDA;
 }

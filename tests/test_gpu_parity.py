@@ -304,3 +304,28 @@ def test_texture_synthesis_deterministic(tiny_spec):
     finally:
         pl.make_schedule = sched
     np.testing.assert_array_equal(a, b)
+
+
+# ---------------------------------------------------------------- final image after 5 iterations
+# SURVEY.md §8(d) parity protocol (3): on <= 5-iteration runs the final image matches the
+# reference's to a mean absolute difference of at most 1/255.
+def test_tinynet_five_iterations_final_image(tiny_spec):
+    d = golden("tinynet.npz")
+    u, v, x = (d[f"case0_{k}"].astype(np.float32) for k in ("u", "v", "x"))
+    p = spst.build_problem(u, v, tiny_spec, spst.default_loss_weights(tiny_spec), block=32, margin=16)
+    x5, tr = spst.minimize(objective_for(p), torch.from_numpy(x).cuda(), spst.LBFGSConfig(history_size=10, max_iters=5))
+    x5 = x5.cpu().numpy() if isinstance(x5, torch.Tensor) else x5
+    np.testing.assert_allclose(tr.losses, d["case0_lbfgs_losses"], rtol=1e-4)
+    assert float(np.mean(np.abs(x5 - d["case0_lbfgs_x5"]))) <= 1.0 / 255
+
+
+def test_vgg19_five_iterations_final_image(vgg_c1):
+    d, p = vgg_c1
+    ref = golden("vgg19_lbfgs5.npz")
+    x5, tr = spst.minimize(objective_for(p), torch.from_numpy(d["c1_u"]).cuda(),
+                           spst.LBFGSConfig(history_size=100, max_iters=5))
+    x5 = x5.cpu().numpy() if isinstance(x5, torch.Tensor) else x5
+    np.testing.assert_allclose(tr.losses, ref["losses"], rtol=2e-3)
+    mad = float(np.mean(np.abs(x5 - ref["x5"])))
+    print(f"VGG C1 5 iterations: final-image mean |diff| {mad:.2e} (bar {1 / 255:.2e})")
+    assert mad <= 1.0 / 255

@@ -24,6 +24,7 @@ sys.path.insert(0, "/root/reference/pkg/src")
 import tilestyle as ts  # noqa: E402
 from tilestyle import extractor as rex, lbfgs as rlb, localized as rloc, pipeline as rpipe  # noqa: E402
 from tilestyle import stats as rst, tensorops as rto, tiling as rti  # noqa: E402
+from tilestyle import metrics as rme  # noqa: E402
 
 from paper_2212_13459_b200 import spec as myspec  # noqa: E402
 from paper_2212_13459_b200.workloads import synth_content, synth_style  # noqa: E402
@@ -226,8 +227,63 @@ def vgg_cases():
     save("vgg19.npz", **d)
 
 
+def metrics_cases():
+    """Reference metrics.py: psnr (24-31), ssim (55-73), gram_distance (76-89)."""
+    d = {}
+    rng = np.random.default_rng(11)
+    pairs = {
+        "rand": (rng.random((64, 80, 3)), None),
+        "min11": (rng.random((11, 11, 3)), None),
+        "gray": (rng.random((40, 53)), None),
+        "synth": (synth_content(151, 129, 5).astype(np.float64), None),
+    }
+    for k, (a, _) in pairs.items():
+        b = np.clip(a + 0.07 * rng.standard_normal(a.shape), 0.0, 1.0)
+        if k == "synth":
+            b = synth_style(151, 129, 6).astype(np.float64)
+        d[f"{k}_a"], d[f"{k}_b"] = a, b
+        d[f"{k}_psnr"] = np.array([rme.psnr(a, b)])
+        d[f"{k}_ssim"] = np.array([rme.ssim(a, b)])
+    # f32 inputs: the reference weights the luma in f32 (NumPy weak scalars)
+    a32 = synth_content(97, 131, 7)
+    b32 = np.clip(a32 + 0.05 * rng.standard_normal(a32.shape).astype(np.float32), 0, 1).astype(np.float32)
+    d["f32_a"], d["f32_b"] = a32, b32
+    d["f32_psnr"], d["f32_ssim"] = np.array([rme.psnr(a32, b32)]), np.array([rme.ssim(a32, b32)])
+    a = d["rand_a"]
+    d["same_psnr"], d["same_ssim"] = np.array([rme.psnr(a, a)]), np.array([rme.ssim(a, a)])
+    # blockwise Gram distance on TinyNet (unweighted and weighted)
+    spec = ts.tinynet(0)
+    x = rng.random((70, 53, 3))
+    v = rng.random((64, 64, 3)) * 0.5 + 0.25
+    d["gd_x"], d["gd_v"] = x, v
+    d["gd_plain"] = np.array([rme.gram_distance(x, v, spec, block=32, margin=16)])
+    w = {t: 1.0 / (i + 1) for i, t in enumerate(spec.style_taps)}
+    d["gd_weighted"] = np.array([rme.gram_distance(x, v, spec, block=32, margin=16, weights=w)])
+    d["gd_weights"] = np.array([w[t] for t in spec.style_taps])
+    save("metrics.npz", **d)
+
+
+def vgg_lbfgs5():
+    """The reference f32 path's first 5 L-BFGS iterations at C1 (final image and losses)."""
+    spec_mine = myspec.calibrated_vgg19(0)
+    spec = to_ref_spec(spec_mine, rex.vgg19("avg"))
+    u = synth_content(256, 256, 1)
+    v = synth_style(256, 256, 2)
+    cfg = rpipe.RunConfig(n_scales=1, extractor=spec)
+    w = rpipe._weights_for_scale(cfg, spec, (256, 256))
+    p32 = rloc.build_problem(u, v, spec, w)
+    t0 = time.time()
+    xr, tr = rlb.minimize(lambda a: rloc.loss_grad(a, p32), u.copy(), rlb.LBFGSConfig(history_size=100, max_iters=5))
+    print(f"reference 5 L-BFGS iters 256^2 f32: {time.time() - t0:.1f}s losses={tr.losses}")
+    save("vgg19_lbfgs5.npz", x5=xr, losses=np.array(tr.losses))
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["kernels", "tiny", "lbfgs", "vgg"]
+    which = sys.argv[1:] or ["kernels", "tiny", "lbfgs", "vgg", "metrics", "lbfgs5"]
+    if "metrics" in which:
+        metrics_cases()
+    if "lbfgs5" in which:
+        vgg_lbfgs5()
     if "kernels" in which:
         kernels()
     if "tiny" in which:

@@ -22,7 +22,7 @@ using namespace spst;
     }                                                                                 \
   } while (0)
 
-enum { SS = 0, TS = 1, PAIR = 2, SSW = 3, TSW = 4 };  // *W: whole warp runs the loop, elect.sync issues
+enum { SS = 0, TS = 1, PAIR = 2, SSW = 3, TSW = 4, SSH = 5, TSH = 6 };  // *H: descriptors hoisted, unrolled x3  // *W: whole warp runs the loop, elect.sync issues
 constexpr int ROWS = 256;            // A rows staged (shift window)
 constexpr int A_BYTES = 2 * ROWS * 16;
 constexpr int B_BYTES = 2 * (256 + 64) * 16;
@@ -137,6 +137,35 @@ __global__ void __launch_bounds__(128, 1) rate_kernel(int R, const uint8_t* nois
       stop = 1;
     }
     __syncwarp();
+  } else if ((MODE == SSH || MODE == TSH) && warp == 0) {
+    const uint32_t idesc = make_idesc_f16(128, N, 0, 0, 0);
+    const uint32_t a0 = smem_u32(sa), b0 = smem_u32(sb);
+    const uint32_t s1 = shift == 1 || shift == 4 ? 1 : shift == 2 ? 8 : 0;
+    const uint64_t ad0 = make_sdesc(a0, ROWS * 16, 128), ad1 = make_sdesc(a0 + s1 * 16, ROWS * 16, 128),
+                   ad2 = make_sdesc(a0 + 2 * s1 * 16, ROWS * 16, 128);
+    const uint32_t t1 = shift == 3 ? 1 : shift == 4 ? 8 : 0;
+    const uint64_t bd0 = make_sdesc(b0, (N + 64) * 16, 128), bd1 = make_sdesc(b0 + t1 * 16, (N + 64) * 16, 128),
+                   bd2 = make_sdesc(b0 + 2 * t1 * 16, (N + 64) * 16, 128);
+    const long long t0 = clock64();
+    for (int i = 0; i < R; i += 3) {
+      if constexpr (MODE == SSH) {
+        umma_f16_elect(tbase, ad0, bd0, idesc, 1u);
+        umma_f16_elect(tbase, ad1, bd1, idesc, 1u);
+        umma_f16_elect(tbase, ad2, bd2, idesc, 1u);
+      } else {
+        umma_f16_ts_elect(tbase, tbase + 256, bd0, idesc, 1u);
+        umma_f16_ts_elect(tbase, tbase + 256, bd1, idesc, 1u);
+        umma_f16_ts_elect(tbase, tbase + 256, bd2, idesc, 1u);
+      }
+    }
+    if (lane == 0) {
+      umma_commit(&done_bar);
+      mbar_wait(&done_bar, 0);
+      const long long t2 = clock64();
+      out_cycles[blockIdx.x] = t2 - t0;
+      stop = 1;
+    }
+    __syncwarp();
   } else if (MODE == PAIR && warp == 0 && lane == 0) {
     mbar_wait(&done_bar, 0);
     out_cycles[blockIdx.x] = 0;
@@ -207,9 +236,9 @@ void run(int R, bool noise, const uint8_t* nsrc, int shift) {
   }
   const double per = (double)mx / R;
   const double floor_c = (MODE == PAIR ? 256.0 : 128.0) * N / (256.0 * (MODE == PAIR ? 2 : 1));
-  const double smem_rd = MODE == TS || MODE == TSW ? N * 32.0 : (MODE == PAIR ? 128 * 32.0 + N / 2 * 32.0 : 128 * 32.0 + N * 32.0);
+  const double smem_rd = MODE == TS || MODE == TSW || MODE == TSH ? N * 32.0 : (MODE == PAIR ? 128 * 32.0 + N / 2 * 32.0 : 128 * 32.0 + N * 32.0);
   printf("shift=%d %-5s N=%3d noise=%d: %7.1f cyc/MMA (math floor %5.1f, eff %5.1f%%), operand smem bytes/MMA %6.0f -> %5.1f B/cyc, noise %5.1f B/cyc\n",
-         shift, MODE == SS ? "SS" : MODE == TS ? "TS" : MODE == SSW ? "SSW" : MODE == TSW ? "TSW" : "PAIR", N, (int)noise, per, floor_c, 100.0 * floor_c / per, smem_rd,
+         shift, MODE == SS ? "SS" : MODE == TS ? "TS" : MODE == SSW ? "SSW" : MODE == TSW ? "TSW" : MODE == SSH ? "SSH" : MODE == TSH ? "TSH" : "PAIR", N, (int)noise, per, floor_c, 100.0 * floor_c / per, smem_rd,
          smem_rd / per, noise ? (double)nsum / cnt / mx : 0.0);
   fflush(stdout);
   CK(cudaFree(cyc));
@@ -221,17 +250,16 @@ int main() {
   CK(cudaMalloc(&nsrc, 64 * 2 * NOISE_CHUNK));
   CK(cudaMemset(nsrc, 0, 64 * 2 * NOISE_CHUNK));
   const int R = 1 << 15;
+  const int RR = 3 * (1 << 13);
   for (int shift = 0; shift < 5; ++shift) {
-    run<64, SS>(R, false, nsrc, shift);
-    run<128, SS>(R, false, nsrc, shift);
-    run<64, SSW>(R, false, nsrc, shift);
-    run<128, SSW>(R, false, nsrc, shift);
-    run<256, SSW>(R, false, nsrc, shift);
-    run<64, TSW>(R, false, nsrc, shift);
-    run<128, TSW>(R, false, nsrc, shift);
+    run<64, SSH>(RR, false, nsrc, shift);
+    run<128, SSH>(RR, false, nsrc, shift);
+    run<256, SSH>(RR, false, nsrc, shift);
+    run<64, TSH>(RR, false, nsrc, shift);
+    run<128, TSH>(RR, false, nsrc, shift);
   }
-  run<128, SSW>(R, true, nsrc, 1);
-  run<64, SSW>(R, true, nsrc, 1);
+  run<64, SSH>(RR, true, nsrc, 1);
+  run<128, SSH>(RR, true, nsrc, 1);
   printf("ok\n");
   return 0;
 }

@@ -213,13 +213,36 @@ class _HostObjective:
         return loss, _as_dev(np.asarray(g, dtype=self.np_dtype), x_dev.device)
 
 
-def minimize(f, x0, cfg: LBFGSConfig, callback=None, allreduce=None):
+@dataclass
+class LBFGSSnapshot:
+    """Everything ``minimize`` needs to continue a run after iteration ``iteration``: the
+    iterate, its gradient and loss, the curvature pairs oldest first with their cached
+    rho = 1/<y,s> and <y,y>, and the trace so far.  Tensors live on the device."""
+    iteration: int
+    x: torch.Tensor
+    g: torch.Tensor
+    loss: float
+    s: list
+    y: list
+    rho: list
+    yy: list
+    losses: list
+    grad_norms: list
+
+
+def minimize(f, x0, cfg: LBFGSConfig, callback=None, allreduce=None, resume: LBFGSSnapshot | None = None,
+             snapshot=None):
     """Minimize f from x0; returns (x, Trace) (lbfgs.py:99-142).
 
     ``f`` may be a reference-style callable on numpy arrays, or a device objective exposing
     ``lazy = True`` with ``loss(x_dev) -> float`` and ``grad(out) -> out`` (gradient of the
     most recent ``loss`` call).  ``allreduce`` (multi-GPU) sums device f64 scalars across
     ranks; vectors are then each rank's shard.
+
+    Mid-run checkpoints (beyond the reference, which resumes only at scale boundaries):
+    ``snapshot=(k, fn)`` calls ``fn(LBFGSSnapshot)`` after every k-th iteration, and
+    ``resume=LBFGSSnapshot`` continues such a run (``x0`` is then ignored) up to
+    ``cfg.max_iters`` total iterations.
     """
     numpy_io = not isinstance(x0, torch.Tensor)
     x = _as_dev(x0).clone()
@@ -262,21 +285,41 @@ def minimize(f, x0, cfg: LBFGSConfig, callback=None, allreduce=None):
             vals = t.tolist()
         return vals[0]
 
-    loss, g = evaluate(x, True, x)
-    gmax = red_max(g)
-    trace.losses.append(loss)
-    trace.grad_norms.append(gmax)
     state = LBFGSState()
-    d = torch.empty_like(x)
-    x_try = torch.empty_like(x)
-    g_spare = torch.empty_like(x) if lazy else None
+    m = cfg.history_size
     # history ring: m+1 preallocated (s, y) slots; the sy kernel writes the candidate pair into
     # the spare slot, so a curvature rejection leaves the stored pairs untouched (lbfgs.py:48-59)
-    m = cfg.history_size
     ring_s = torch.empty((m + 1,) + tuple(x.shape), dtype=x.dtype, device=x.device)
     ring_y = torch.empty_like(ring_s)
     slot_of = []  # ring slot of each stored pair, oldest first
-    for it in range(cfg.max_iters):
+    first_it = 0
+    if resume is None:
+        loss, g = evaluate(x, True, x)
+        gmax = red_max(g)
+        trace.losses.append(loss)
+        trace.grad_norms.append(gmax)
+    else:
+        if len(resume.s) > m:
+            raise ValueError(f"snapshot holds {len(resume.s)} pairs, history_size is {m}")
+        x.copy_(_as_dev(resume.x).to(x.dtype))
+        g = _as_dev(resume.g).to(device=x.device, dtype=x.dtype).clone()
+        loss = float(resume.loss)
+        for k, (sk, yk) in enumerate(zip(resume.s, resume.y)):
+            ring_s[k].copy_(_as_dev(sk))
+            ring_y[k].copy_(_as_dev(yk))
+            state.s_hist.append(ring_s[k])
+            state.y_hist.append(ring_y[k])
+            state.rho.append(float(resume.rho[k]))
+            state.yy.append(float(resume.yy[k]))
+            slot_of.append(k)
+        first_it = state.iter = int(resume.iteration)
+        trace.losses.extend(float(v) for v in resume.losses)
+        trace.grad_norms.extend(float(v) for v in resume.grad_norms)
+        gmax = red_max(g)
+    d = torch.empty_like(x)
+    x_try = torch.empty_like(x)
+    g_spare = torch.empty_like(x) if lazy else None
+    for it in range(first_it, cfg.max_iters):
         if gmax <= cfg.grad_tol:
             break
         _two_loop(g, state, vec, d, allreduce)
@@ -325,4 +368,8 @@ def minimize(f, x0, cfg: LBFGSConfig, callback=None, allreduce=None):
         trace.grad_norms.append(gmax)
         if callback is not None:
             callback(it + 1, host_x(x) if numpy_io else x, loss, gmax)
+        if snapshot is not None and (it + 1) % snapshot[0] == 0:
+            snapshot[1](LBFGSSnapshot(iteration=it + 1, x=x, g=g, loss=loss, s=list(state.s_hist),
+                                      y=list(state.y_hist), rho=list(state.rho), yy=list(state.yy),
+                                      losses=list(trace.losses), grad_norms=list(trace.grad_norms)))
     return (x.cpu().numpy() if numpy_io else x), trace

@@ -140,16 +140,28 @@ def run_ours(args):
     if world > 1:
         import torch.distributed as tdist
 
+    # the native engine of this rank: its launch timer brackets every tensor-core launch with
+    # CUDA events on the engine stream during the timed iterations (dominant-kernel roofline)
+    eng = getattr(problem, "engine", None)
+    eng = getattr(eng, "e", eng)
+    if not hasattr(eng, "timing_enable"):
+        eng = None
+
     def on_iter(it, xi, loss, gnorm):
         if it in (args.warmup, args.warmup + args.steps):
             torch.cuda.synchronize()
             if world > 1:
                 tdist.barrier()
             if it == args.warmup:
+                if eng is not None:
+                    eng.timing_enable(True)
                 sampler.start()
                 e0.record()
             else:
                 e1.record()
+                if eng is not None:
+                    marks["timer"] = eng.timing_read()
+                    eng.timing_enable(False)
             marks[it] = None
 
     x, tr_all = minimize(objective, x, LBFGSConfig(history_size=10, max_iters=args.warmup + args.steps),
@@ -209,18 +221,45 @@ def run_ours(args):
                        "image": [H, W], "style": [sh, sw], "history": 10, "parallelism": f"row-stripes x{world}",
                        "l2_flush": "not needed (working set ~80 GB >> 126 MB L2)",
                        "evals_per_iter": evals_per_iter, "setup_s": setup_s},
-            "roofline": {"bound": "tensor", "kernel": "conv3x3_tc (fwd+bwd) + gram_tc, per loss_grad eval",
-                         "achieved": achieved, "peak": peak_sus, "unit": "TFLOP/s",
-                         "frac": (achieved / peak_sus) if achieved else None, "traffic": None,
-                         "peak_kind": f"bf16 dense sustained ({peak_kind})",
-                         "algorithmic_flop_per_eval": flops_eval, "eval_ms": eval_ms,
-                         "note": "algorithmic FLOPs (1 pass); fp16x3 executes 3 MMA passes"},
+            "roofline": dominant_roofline(marks.get("timer"), ms, peak_sus, peak_kind, flops_eval, eval_ms, world),
             "e2e": e2e,
             "cpu_baseline": cpu,
             "gpu_launches": n_launch,
             "clocks": clocks,
         }
         print(json.dumps(line))
+
+
+def dominant_roofline(timer, step_region_ms, peak, peak_kind, flops_eval, eval_ms, world):
+    """Roofline of the dominant kernel class from the engine's live launch timer: achieved =
+    algorithmic FLOPs of its launches / their summed device time (CUDA events on the launching
+    stream over the timed region); traffic = DRAM bytes per launch from the committed ncu
+    capture (profiles/), or None."""
+    whole = {"achieved_per_eval": (flops_eval / (eval_ms / 1e3) / 1e12 / world) if eval_ms else None,
+             "algorithmic_flop_per_eval": flops_eval, "eval_ms": eval_ms}
+    if not timer:
+        return {"bound": "tensor", "kernel": "whole loss_grad eval (launch timer unavailable)",
+                "achieved": whole["achieved_per_eval"], "peak": peak, "unit": "TFLOP/s",
+                "frac": (whole["achieved_per_eval"] / peak) if whole["achieved_per_eval"] else None,
+                "traffic": None, "peak_kind": peak_kind, **whole}
+    name, (kms, kflops, n) = max(timer.items(), key=lambda kv: kv[1][0])
+    achieved = kflops / (kms / 1e3) / 1e12
+    traffic = None
+    try:
+        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "dominant_traffic.json")) as f:
+            tr = json.load(f)
+        if tr.get("kernel_class") == name:
+            traffic = tr["dram_bytes_per_launch"]
+    except (OSError, ValueError, KeyError):
+        pass
+    return {"bound": "tensor", "kernel": name, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+            "frac": achieved / peak, "traffic": traffic, "traffic_unit": "bytes DRAM per launch (ncu)",
+            "peak_kind": f"bf16 dense sustained ({peak_kind})",
+            "launches": n, "avg_launch_ms": kms / n, "algorithmic_flop_per_launch": kflops / n,
+            "share_of_timed_region": kms / step_region_ms,
+            "classes": {c: {"ms": v[0], "tflop": v[1] / 1e12, "launches": v[2]} for c, v in timer.items()},
+            "note": "algorithmic FLOPs (real channels, 1 pass); the fp16x3 split executes 3 MMA passes, "
+                    "so frac <= 1/3 by construction", **whole}
 
 
 def measure_eval(objective, x, torch):
@@ -328,7 +367,10 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c4")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--ref-evals-per-iter", type=float, default=2.0)
+    # the reference's line search is restated exactly by ours, so trials per iteration are a
+    # property of the problem: 1.08 is what our minimize measures at C4 (the reference itself
+    # measured 1.8 at the 256^2 C1 config)
+    ap.add_argument("--ref-evals-per-iter", type=float, default=1.08)
     ap.add_argument("--cpu-block", type=int, default=1024, help="CPU sample block side (padded px)")
     args = ap.parse_args()
     if args.impl == "reference":

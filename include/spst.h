@@ -98,6 +98,15 @@ int spst_finalize(spst_ctx* ctx, const long long* n, double* terms_host, int* de
  * two_lambda = 2 * lambda_c (0 disables the content term). */
 int spst_backward(spst_ctx* ctx, double two_lambda, float* grad_dev);
 
+/* ---------------------------------------------------------------- launch timer ---------
+ * Measurement hook (no reference counterpart): when enabled, every tensor-core launch is
+ * bracketed by CUDA events on the context stream.  spst_timing_read returns, per class
+ * (0 conv3x3_tc N=128, 1 conv3x3_tc N=64, 2 Gram, 3 unused), the summed device ms, the
+ * algorithmic FLOPs of those launches (real channel counts, one pass) and the launch count.
+ * spst_timing_enable resets the totals. */
+int spst_timing_enable(spst_ctx* ctx, int on);
+int spst_timing_read(spst_ctx* ctx, double* ms4, double* flops4, long long* launches4);
+
 /* ---------------------------------------------------------------- vector kernels ---------
  * lbfgs.py:68-142. Reductions accumulate in f64 with a fixed order (deterministic). The
  * partial buffer must hold spst_vec_partials() doubles per reduced quantity. */

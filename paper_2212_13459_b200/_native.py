@@ -63,6 +63,8 @@ SIGNATURES = {
     "spst_vec_axpy": (c_int, [c_int, c_void_p, c_void_p, c_double, c_longlong, c_void_p, c_void_p]),
     "spst_vec_sy": (c_int, [c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_longlong, c_void_p, c_void_p,
                             c_void_p, c_void_p, c_void_p]),
+    "spst_timing_enable": (c_int, [c_void_p, c_int]),
+    "spst_timing_read": (c_int, [c_void_p, POINTER(c_double), POINTER(c_double), POINTER(c_longlong)]),
     "spst_metric_sqdiff": (c_int, [c_int, c_void_p, c_void_p, c_longlong, c_void_p, c_void_p, c_void_p]),
     "spst_metric_ssim": (c_int, [c_int, c_void_p, c_void_p, c_int, c_int, c_int, c_void_p, c_void_p, c_void_p]),
     "spst_resize_down": (c_int, [c_void_p, c_int, c_int, c_int, c_int, c_void_p, c_void_p]),

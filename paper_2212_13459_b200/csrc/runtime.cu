@@ -132,6 +132,9 @@ struct TapState {
   double* colsum_mid = nullptr;
 };
 
+// launch-timer classes: 0 conv3x3_tc N=128, 1 conv3x3_tc N=64, 2 Gram (tc kernel + reduce)
+constexpr int kTimerClasses = 4;
+
 struct Expo {
   int e = 0;
   bool known = false;
@@ -177,6 +180,17 @@ struct spst_ctx {
   unsigned int* amax_d = nullptr;  // [stages][4]: out, pooled, grad, addend; [4 * stages]: image
   HL16 img;                        // first conv's K operand (8-channel HL16 image), see image_hl_kernel
   Expo img_e;
+  // opt-in launch timer (spst_timing_*): CUDA events around each tensor-core launch on `stream`
+  struct LaunchTimer {
+    cudaEvent_t a = nullptr, b = nullptr;
+    int cls = 0;
+    double flops = 0;
+  };
+  bool timing = false;
+  std::vector<LaunchTimer> tpool;
+  size_t tused = 0;
+  double t_ms[kTimerClasses] = {}, t_flops[kTimerClasses] = {};
+  long long t_n[kTimerClasses] = {};
   std::vector<unsigned int> amax_h;
   HL16 gbuf[2];
   size_t gbuf_elems = 0;
@@ -383,8 +397,39 @@ struct ConvLaunch {
   int n_xkc = 0;
   int H = 0, W = 0;              // GEMM grid (conv output grid)
   float acc_scale = 1.f;
+  double flops = 0;              // algorithmic FLOPs (real channels, one pass) for the launch timer
   ConvArgs a{};
 };
+
+spst_ctx::LaunchTimer* timer_begin(spst_ctx* ctx, int cls, double flops) {
+  if (!ctx->timing) return nullptr;
+  if (ctx->tused == ctx->tpool.size()) {
+    spst_ctx::LaunchTimer t;
+    if (cudaEventCreate(&t.a) != cudaSuccess || cudaEventCreate(&t.b) != cudaSuccess) return nullptr;
+    ctx->tpool.push_back(t);
+  }
+  spst_ctx::LaunchTimer* t = &ctx->tpool[ctx->tused++];
+  t->cls = cls;
+  t->flops = flops;
+  cudaEventRecord(t->a, ctx->stream);
+  return t;
+}
+void timer_end(spst_ctx* ctx, spst_ctx::LaunchTimer* t) {
+  if (t) cudaEventRecord(t->b, ctx->stream);
+}
+// fold the recorded launches into the per-class totals (the stream has been synchronized)
+void timer_collect(spst_ctx* ctx) {
+  for (size_t i = 0; i < ctx->tused; ++i) {
+    const auto& t = ctx->tpool[i];
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, t.a, t.b) == cudaSuccess) {
+      ctx->t_ms[t.cls] += ms;
+      ctx->t_flops[t.cls] += t.flops;
+      ctx->t_n[t.cls] += 1;
+    }
+  }
+  ctx->tused = 0;
+}
 
 int run_conv(spst_ctx* ctx, ConvLaunch& L) {
   ConvArgs& a = L.a;
@@ -417,7 +462,9 @@ int run_conv(spst_ctx* ctx, ConvLaunch& L) {
   int cs = cluster_mode;
   while (cs > 1 && a.tiles_x * a.tiles_y < 4 * cs) cs /= 2;
   const int grid = std::min(tiles, (kSMs / std::max(cs, 1)) * std::max(cs, 1));
+  auto* tm = timer_begin(ctx, N == 128 ? 0 : 1, L.flops);
   CK(launch_conv_tc(a, N, std::max(grid, cs), ctx->stream, cs));
+  timer_end(ctx, tm);
   return SPST_OK;
 }
 
@@ -464,6 +511,7 @@ int forward_stage(spst_ctx* ctx, int k, const float* x) {
   L.H = s.H;
   L.W = s.W;
   L.acc_scale = 1.f / (in.scale * pow2f(s.wexp));
+  L.flops = 2.0 * s.H * s.W * s.cout * 9.0 * s.cin;
   ConvArgs& a = L.a;
   a.epi = s.pool_after ? EPI_FWD_POOL : EPI_FWD;
   a.bias = s.bias_d;
@@ -497,12 +545,14 @@ int stage_stats(spst_ctx* ctx, int k) {
   g.n_ctile = (s.cout_p + 127) / 128;
   g.partial = t.gram_partial;
   const double inv2 = 1.0 / ((double)s.out.scale * (double)s.out.scale);
+  auto* tm = timer_begin(ctx, 2, 2.0 * (double)(p1 - p0) * s.cout * s.cout);
   if (s.cout_p == 64) {
     CK(launch_gram64_tc(g, t.gram_splits, s.cout, inv2, t.S, ctx->stream));
   } else {
     CK(launch_gram_tc(g, t.gram_splits, ctx->stream));
     CK(launch_gram_reduce(t.gram_partial, t.gram_splits, g.n_ctile, s.cout, inv2, t.S, ctx->stream));
   }
+  timer_end(ctx, tm);
   return SPST_OK;
 }
 
@@ -539,6 +589,7 @@ int do_forward(spst_ctx* ctx, const float* x, bool careful) {
   ctx->amax_h.resize(4 * n + 4);
   CK(cudaMemcpyAsync(ctx->amax_h.data(), ctx->amax_d, 16 * n + 16, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
+  timer_collect(ctx);
   bool bad = false;
   {
     const float mi = bits_to_float(ctx->amax_h[4 * n]);
@@ -619,6 +670,7 @@ int tap_grad_gemm(spst_ctx* ctx, int k, HL16 out, bool with_mask, double two_lam
   L.H = s.H;
   L.W = s.W;
   L.acc_scale = 1.f / (s.out.scale * pow2f(xexp));
+  L.flops = s.style >= 0 ? 2.0 * s.H * s.W * s.cout * s.cout : 0.0;  // style GEMM V M (content-only: none)
   ConvArgs& a = L.a;
   a.x_rescale = 1.f;
   a.epi = EPI_BWD;
@@ -651,6 +703,7 @@ int backward_stage(spst_ctx* ctx, int k, int src, int dst, double two_lambda) {
   L.W = nx.W;
   const int acc_e = nx.g_e.e + nx.wexp;
   L.acc_scale = 1.f / pow2f(acc_e);
+  L.flops = 2.0 * nx.H * nx.W * nx.cin * 9.0 * nx.cout;  // input-gradient GEMM of conv k+1
   ConvArgs& a = L.a;
   a.x_rescale = 1.f;
   a.out = gout;
@@ -670,6 +723,7 @@ int backward_stage(spst_ctx* ctx, int k, int src, int dst, double two_lambda) {
       L.v = &s.out;
       L.xw = ctx->taps[s.style].xw;
       L.n_xkc = s.cout_p / 32;
+      L.flops += 2.0 * s.H * s.W * s.cout * s.cout;  // fused style GEMM V M
       a.x_rescale = (float)std::ldexp(1.0, acc_e - xexp) / s.out.scale;
       a.bias = ctx->taps[s.style].bvec;
     }
@@ -753,15 +807,11 @@ int do_backward(spst_ctx* ctx, double two_lambda, float* grad, bool careful) {
   const int r0 = ctx->own_r0, r1 = std::min(ctx->own_r1, ctx->h);
   CK(launch_fold_grad(ctx->gimg, s0.H, s0.W, ctx->grid_r0, ctx->h, ctx->w, r0, r1, grad, ctx->stream));
   // end-of-pass range check (fast path)
-  ctx->amax_h.resize(4 * n + 4);
-  CK(cudaMemcpyAsync(ctx->amax_h.data(), ctx->amax_d, 16 * n + 16, cudaMemcpyDeviceToHost, ctx->stream));
+  ctx->amax_h.resize(4 * n);
+  CK(cudaMemcpyAsync(ctx->amax_h.data(), ctx->amax_d, 16 * n, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
+  timer_collect(ctx);
   bool bad = false;
-  {
-    const float mi = bits_to_float(ctx->amax_h[4 * n]);
-    if (!std::isfinite(mi) || mi * ctx->img.scale > kOverflow) bad = true;
-    if (mi > 0 && std::isfinite(mi)) ctx->img_e = {choose_exp(mi), true};
-  }
   for (int k = 0; k < n; ++k) {
     Stage& s = ctx->stages[k];
     const float m = bits_to_float(ctx->amax_h[4 * k + 2]);
@@ -957,12 +1007,37 @@ int spst_create(int device, int n_layers, const int* kinds, const int* cin, cons
 
 void spst_destroy(spst_ctx* ctx) {
   if (!ctx) return;
+  for (auto& t : ctx->tpool) {
+    cudaEventDestroy(t.a);
+    cudaEventDestroy(t.b);
+  }
   ctx->release_bound();
   for (void* p : ctx->persistent) cudaFree(p);
   delete ctx;
 }
 
 const char* spst_last_error(const spst_ctx* ctx) { return ctx ? ctx->msg.c_str() : "null context"; }
+
+int spst_timing_enable(spst_ctx* ctx, int on) {
+  if (!ctx) return SPST_ERR_CONFIG;
+  if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return SPST_ERR_CUDA;
+  ctx->tused = 0;
+  for (int c = 0; c < kTimerClasses; ++c) ctx->t_ms[c] = ctx->t_flops[c] = 0, ctx->t_n[c] = 0;
+  ctx->timing = on != 0;
+  return SPST_OK;
+}
+
+int spst_timing_read(spst_ctx* ctx, double* ms, double* flops, long long* launches) {
+  if (!ctx) return SPST_ERR_CONFIG;
+  if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return SPST_ERR_CUDA;
+  timer_collect(ctx);
+  for (int c = 0; c < kTimerClasses; ++c) {
+    ms[c] = ctx->t_ms[c];
+    flops[c] = ctx->t_flops[c];
+    launches[c] = ctx->t_n[c];
+  }
+  return SPST_OK;
+}
 
 int spst_set_stream(spst_ctx* ctx, void* stream) {
   ctx->stream = reinterpret_cast<cudaStream_t>(stream);

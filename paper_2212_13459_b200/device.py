@@ -198,6 +198,18 @@ class Engine:
             out[self.spec.layers[li + 1].name] = buf.astype(bool)
         return out
 
+    TIMER_CLASSES = ("conv3x3_tc<128>", "conv3x3_tc<64>", "gram_tc", "unused")
+
+    def timing_enable(self, on=True):
+        """Bracket every tensor-core launch with CUDA events on the engine stream (resets totals)."""
+        self._check(nat.lib().spst_timing_enable(self._h, 1 if on else 0), "spst_timing_enable")
+
+    def timing_read(self):
+        """{class: (device ms, algorithmic FLOPs, launches)} since timing_enable."""
+        ms, fl, n = (ctypes.c_double * 4)(), (ctypes.c_double * 4)(), (ctypes.c_longlong * 4)()
+        self._check(nat.lib().spst_timing_read(self._h, ms, fl, n), "spst_timing_read")
+        return {c: (ms[i], fl[i], n[i]) for i, c in enumerate(self.TIMER_CLASSES) if n[i]}
+
     def backward(self, two_lambda, grad_dev):
         self.stream()
         with torch.cuda.device(self.device):

@@ -59,8 +59,8 @@ __device__ __forceinline__ void umma_f16_ts_elect(uint32_t tmem_d, uint32_t tmem
 // shift: 0 none, 1 A by 0..2 rows (16 B steps, the conv's dx taps), 2 A by 8-row steps (128 B),
 // 3 B by 0..2 rows, 4 A by 0..2 rows and B by 8-row steps
 template <int N, int MODE>
-__global__ void __launch_bounds__(128, 1) rate_kernel(int R, const uint8_t* noise_src, long long* out_cycles,
-                                                      long long* out_noise, int shift) {
+__global__ void __launch_bounds__(384, 1) rate_kernel(int R, const uint8_t* noise_src, long long* out_cycles,
+                                                      long long* out_noise, int shift, int lsu, uint4* gdst) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sa = smem;
@@ -170,6 +170,30 @@ __global__ void __launch_bounds__(128, 1) rate_kernel(int R, const uint8_t* nois
     mbar_wait(&done_bar, 0);
     out_cycles[blockIdx.x] = 0;
     stop = 1;
+  } else if (warp >= 2 && lsu) {
+    // LSU noise: lsu=1 st.global.v4 (coalesced 512 B per warp), 2 ld.shared.v4, 3 local spills
+    long long n = 0;
+    uint4 v = make_uint4(threadIdx.x, 1, 2, 3);
+    const size_t base = ((size_t)blockIdx.x * 320 + (threadIdx.x - 64)) ;
+    const uint4* sh = reinterpret_cast<const uint4*>(sn);
+    uint4 loc[24];
+    for (int i = 0; i < 24; ++i) loc[i] = v;
+    while (!stop) {
+#pragma unroll 4
+      for (int k = 0; k < 64; ++k) {
+        if (lsu == 1) gdst[(base + (size_t)k * 148 * 320) & ((1u << 22) - 1)] = v;
+        else if (lsu == 2) {
+          uint4 t;
+          asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(t.x), "=r"(t.y), "=r"(t.z), "=r"(t.w)
+                       : "r"(smem_u32(sh + ((threadIdx.x * 7 + k * 32) & 2047))));
+          v.x += t.x;
+        }
+        else { loc[(k + v.x) % 24].y += v.x; v.x += loc[(k * 5 + v.y) % 24].x; }
+      }
+      n += 64;
+    }
+    if (v.x == 12345u) out_noise[0] = v.y + loc[3].y;
+    if (lane == 0 && warp == 2) out_noise[blockIdx.x] = n;
   } else if (warp == 1 && lane == 0 && noise_src) {
     long long bytes = 0;
     uint32_t ph = 0;
@@ -198,8 +222,9 @@ __global__ void __launch_bounds__(128, 1) rate_kernel(int R, const uint8_t* nois
   }
 }
 
+static uint4* g_dst = nullptr;
 template <int N, int MODE>
-void run(int R, bool noise, const uint8_t* nsrc, int shift) {
+void run(int R, bool noise, const uint8_t* nsrc, int shift, int lsu = 0) {
   auto k = rate_kernel<N, MODE>;
   const int smem = A_BYTES + B_BYTES + 2 * NOISE_CHUNK + 1024;
   CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -211,7 +236,7 @@ void run(int R, bool noise, const uint8_t* nsrc, int shift) {
   CK(cudaMemset(nb, 0, grid * 8));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(128);
+  cfg.blockDim = dim3(lsu ? 384 : 128);
   cfg.dynamicSmemBytes = smem;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -220,7 +245,7 @@ void run(int R, bool noise, const uint8_t* nsrc, int shift) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  for (int rep = 0; rep < 2; ++rep) CK(cudaLaunchKernelEx(&cfg, k, R, noise ? nsrc : nullptr, cyc, nb, shift));
+  for (int rep = 0; rep < 2; ++rep) CK(cudaLaunchKernelEx(&cfg, k, R, noise ? nsrc : nullptr, cyc, nb, shift, lsu, g_dst));
   CK(cudaDeviceSynchronize());
   std::vector<long long> hc(grid), hn(grid);
   CK(cudaMemcpy(hc.data(), cyc, grid * 8, cudaMemcpyDeviceToHost));
@@ -237,8 +262,8 @@ void run(int R, bool noise, const uint8_t* nsrc, int shift) {
   const double per = (double)mx / R;
   const double floor_c = (MODE == PAIR ? 256.0 : 128.0) * N / (256.0 * (MODE == PAIR ? 2 : 1));
   const double smem_rd = MODE == TS || MODE == TSW || MODE == TSH ? N * 32.0 : (MODE == PAIR ? 128 * 32.0 + N / 2 * 32.0 : 128 * 32.0 + N * 32.0);
-  printf("shift=%d %-5s N=%3d noise=%d: %7.1f cyc/MMA (math floor %5.1f, eff %5.1f%%), operand smem bytes/MMA %6.0f -> %5.1f B/cyc, noise %5.1f B/cyc\n",
-         shift, MODE == SS ? "SS" : MODE == TS ? "TS" : MODE == SSW ? "SSW" : MODE == TSW ? "TSW" : MODE == SSH ? "SSH" : MODE == TSH ? "TSH" : "PAIR", N, (int)noise, per, floor_c, 100.0 * floor_c / per, smem_rd,
+  printf("lsu=%d shift=%d %-5s N=%3d noise=%d: %7.1f cyc/MMA (math floor %5.1f, eff %5.1f%%), operand smem bytes/MMA %6.0f -> %5.1f B/cyc, noise %5.1f B/cyc\n",
+         lsu, shift, MODE == SS ? "SS" : MODE == TS ? "TS" : MODE == SSW ? "SSW" : MODE == TSW ? "TSW" : MODE == SSH ? "SSH" : MODE == TSH ? "TSH" : "PAIR", N, (int)noise, per, floor_c, 100.0 * floor_c / per, smem_rd,
          smem_rd / per, noise ? (double)nsum / cnt / mx : 0.0);
   fflush(stdout);
   CK(cudaFree(cyc));
@@ -251,15 +276,12 @@ int main() {
   CK(cudaMemset(nsrc, 0, 64 * 2 * NOISE_CHUNK));
   const int R = 1 << 15;
   const int RR = 3 * (1 << 13);
-  for (int shift = 0; shift < 5; ++shift) {
-    run<64, SSH>(RR, false, nsrc, shift);
-    run<128, SSH>(RR, false, nsrc, shift);
-    run<256, SSH>(RR, false, nsrc, shift);
-    run<64, TSH>(RR, false, nsrc, shift);
-    run<128, TSH>(RR, false, nsrc, shift);
+  CK(cudaMalloc(&g_dst, (size_t)16 << 22));
+  for (int lsu = 0; lsu < 4; ++lsu) {
+    run<128, SSH>(RR, false, nsrc, 1, lsu);
+    run<64, SSH>(RR, false, nsrc, 1, lsu);
+    run<128, TSH>(RR, false, nsrc, 1, lsu);
   }
-  run<64, SSH>(RR, true, nsrc, 1);
-  run<128, SSH>(RR, true, nsrc, 1);
   printf("ok\n");
   return 0;
 }

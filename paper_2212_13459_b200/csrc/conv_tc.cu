@@ -64,6 +64,33 @@ __device__ __forceinline__ bool chunk_is_extra(int c, int n_kc, int& idx) {
   return e;
 }
 
+// TMEM accumulation groups: up to D consecutive chunks of the same kind (conv / extra-K,
+// which carry different scales) share one fresh TMEM buffer before the epilogue drains it.
+// Two 16-channel chunks per buffer double the MMA's lead over the per-tile epilogue and halve
+// the drain work, at ~2x the (fp32-class) in-TMEM accumulation error of a single chunk.
+// Only the N=128 kernel needs the longer lead (NBUF=2); N=64 has 4 buffers and keeps one chunk
+// per buffer (its full-resolution layers feed every deeper one).
+// Build with -DSPST_CONV_DRAIN=1 for one chunk per buffer everywhere (~3x smaller in-TMEM
+// accumulation error, ~7% slower evaluation; measured in DESIGN.md §5).
+#ifndef SPST_CONV_DRAIN
+#define SPST_CONV_DRAIN 2
+#endif
+template <int N>
+struct DrainCfg {
+  static constexpr int D = N == 128 ? SPST_CONV_DRAIN : 1;
+};
+template <int D>
+__device__ __forceinline__ void chunk_group(int c, int n_kc, int n_chunks, bool& first, bool& last) {
+  const int j = c < n_kc ? c : c - n_kc;
+  const int end = c < n_kc ? n_kc : n_chunks;
+  first = j % D == 0;
+  last = j % D == D - 1 || c == end - 1;
+}
+template <int D>
+__host__ __device__ constexpr int n_groups(int n_kc, int n_xkc) {
+  return (n_kc + D - 1) / D + (n_xkc + D - 1) / D;
+}
+
 __device__ __forceinline__ void store_hl8(const HL16& t, int kg, int y, int x, const float* v8, float s) {
   __align__(16) __half h[8];
   __align__(16) __half l[8];
@@ -376,11 +403,13 @@ __global__ void __launch_bounds__(320, 1) conv3x3_tc_kernel(const __grid_constan
     // one elected lane issues; see umma_f16_ws)
     {
       const uint32_t idesc = make_idesc_f16(128, N, 0, 0, 0);
-      uint32_t g = 0;
+      uint32_t g = 0, gq = 0;  // chunk counter (smem stages), group counter (TMEM buffers)
       for (int t = first; t < n_tiles; t += step) {
         for (int c = 0; c < n_chunks; ++c, ++g) {
-          const uint32_t b = g % C::NBUF;
-          mbar_wait(&cempty_bar[b], ((g / C::NBUF) & 1) ^ 1);
+          bool gfirst, glast;
+          chunk_group<DrainCfg<N>::D>(c, a.n_kc, n_chunks, gfirst, glast);
+          const uint32_t b = gq % C::NBUF;
+          if (gfirst) mbar_wait(&cempty_bar[b], ((gq / C::NBUF) & 1) ^ 1);
           const int s = g % C::STAGES;
           mbar_wait(&full_bar[s], (g / C::STAGES) & 1);
           __syncwarp();
@@ -404,7 +433,7 @@ __global__ void __launch_bounds__(320, 1) conv3x3_tc_kernel(const __grid_constan
                 for (int mt = 0; mt < C::MT; ++mt) {
                   const uint64_t ad =
                       adesc0 + (uint64_t)(((pass == 1 ? C::XA_HALF : 0) + mt * 128 * 16 + 2 * ks * C::XA_PLANE) >> 4);
-                  umma_f16_ws(dcol + mt * N, ad, bd, idesc, (pass | ks) ? 1u : 0u);
+                  umma_f16_ws(dcol + mt * N, ad, bd, idesc, (!gfirst || pass | ks) ? 1u : 0u);
                 }
               }
           } else {
@@ -424,7 +453,7 @@ __global__ void __launch_bounds__(320, 1) conv3x3_tc_kernel(const __grid_constan
 #pragma unroll
                 for (int mt = 0; mt < C::MT; ++mt) {
                   const uint64_t ad = ap + (uint64_t)((((mt + dy) * C::PITCH + dx) * 16) >> 4);
-                  umma_f16_ws(dcol + mt * N, ad, bd, idesc, (pass | tap) ? 1u : 0u);  // fresh per chunk
+                  umma_f16_ws(dcol + mt * N, ad, bd, idesc, (!gfirst || pass | tap) ? 1u : 0u);  // fresh per group
                 }
               }
             }
@@ -433,7 +462,10 @@ __global__ void __launch_bounds__(320, 1) conv3x3_tc_kernel(const __grid_constan
             umma_commit_multicast_ws(&empty_bar[s], kMask);  // release the stage in every CTA
           else
             umma_commit_ws(&empty_bar[s]);
-          umma_commit_ws(&cfull_bar[b]);
+          if (glast) {
+            umma_commit_ws(&cfull_bar[b]);
+            ++gq;
+          }
         }
       }
     }
@@ -453,13 +485,14 @@ __global__ void __launch_bounds__(320, 1) conv3x3_tc_kernel(const __grid_constan
       float acc0[C::CPG], acc1[C::CPG];
 #pragma unroll
       for (int i = 0; i < C::CPG; ++i) acc0[i] = acc1[i] = 0.f;
-      for (int c = 0; c < n_chunks; ++c, ++g) {
+      constexpr int D = DrainCfg<N>::D;
+      const int n_conv_groups = (a.n_kc + D - 1) / D;
+      for (int c = 0; c < n_groups<D>(a.n_kc, a.n_xkc); ++c, ++g) {
         const uint32_t b = g % C::NBUF;
         mbar_wait(&cfull_bar[b], (g / C::NBUF) & 1);
         tc_fence_after();
         const uint32_t trow = tmem_base + ((q * 32u) << 16) + b * C::MT * N + 2 * rp * N + cofs;
-        int ci;
-        const float cs = chunk_is_extra(c, a.n_kc, ci) ? a.x_rescale : 1.f;  // own scale
+        const float cs = c >= n_conv_groups ? a.x_rescale : 1.f;  // extra-K groups carry their own scale
         if constexpr (C::CPG == 32) {  // both rows in one batch: 2 loads, 1 wait
           float v0[32], v1[32];
           tmem_ld32x2(trow, trow + N, v0, v1);

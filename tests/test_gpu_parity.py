@@ -144,9 +144,18 @@ def test_vgg19_loss_grad_vs_reference_f64(vgg_c1):
     assert arith <= 1e-4
     assert tie <= 1e-4
     assert err <= 2e-2
+    # x1: the reference's first line-search trial point (away from x0's near-zero structure)
     loss1, g1 = spst.loss_grad(d["c1_x1"], p)
     assert abs(loss1 - d["c1_loss64_x1"][0]) <= 1e-4 * d["c1_loss64_x1"][0]
-    assert rel_l2(g1, d["c1_grad64_x1"]) <= 1e-3
+    masks1 = p.engine.relu_masks()
+    _, gm1 = O.loss_grad_global(d["c1_x1"].astype(np.float64), po, masks=masks1)
+    flips1, tie1 = _flips(masks1, _f64_preacts(po, d["c1_x1"]))
+    err1, arith1 = rel_l2(g1, d["c1_grad64_x1"]), rel_l2(g1, gm1)
+    print(f"x1: grad rel-L2 vs f64 {err1:.2e}; vs f64-on-our-masks {arith1:.2e}; ReLU flips {flips1} "
+          f"(max |pre|/rms {tie1:.1e})")
+    assert arith1 <= 1e-4
+    assert tie1 <= 1e-4
+    assert err1 <= 2e-2
 
 
 def test_vgg19_ragged_dims_vs_reference_f64(vgg_spec):
@@ -156,7 +165,19 @@ def test_vgg19_ragged_dims_vs_reference_f64(vgg_spec):
     loss, g = spst.loss_grad(d["r_x"], p)
     assert g.shape == (72, 88, 3)
     assert abs(loss - d["r_loss64"][0]) <= 1e-4 * d["r_loss64"][0]
-    assert rel_l2(g, d["r_grad64"]) <= 1e-3
+    # replicate padding + fold on ragged dims; arithmetic on our ReLU pattern, flips near-ties
+    net = O.onet_from_spec(vgg_spec)
+    po = O.build_problem(d["r_u"].astype(np.float64), d["r_v"].astype(np.float64), net,
+                         O.default_weights(net, float(d["r_lambda_c"][0])), 512, 256)
+    masks = p.engine.relu_masks()
+    _, gm = O.loss_grad_global(d["r_x"].astype(np.float64), po, masks=masks)
+    flips, tie = _flips(masks, _f64_preacts(po, d["r_x"]))
+    err, arith = rel_l2(g, d["r_grad64"]), rel_l2(g, gm)
+    print(f"ragged: grad rel-L2 vs f64 {err:.2e}; vs f64-on-our-masks {arith:.2e}; ReLU flips {flips} "
+          f"(max |pre|/rms {tie:.1e})")
+    assert arith <= 1e-4
+    assert tie <= 1e-4
+    assert err <= 2e-2
 
 
 def test_vgg19_lbfgs_same_x_first_five_iterates(vgg_spec, vgg_c1):

@@ -41,7 +41,10 @@ struct ConvCfg {
   static constexpr int A_BYTES = 2 * A_HALF;        // hi + lo
   static constexpr int B_TAP = 2 * N * 16;          // 16 channels x N outputs (fp16)
   static constexpr int B_BYTES = 2 * 9 * B_TAP;     // hi/lo x 9 taps
-  static constexpr int XKG = 8 / MT;                // extra-K chunk: 32 (MT=2) or 16 (MT=4) channels
+  // extra-K (style-gradient) chunk: 8*XKG channels of the tap features at the tile's own pixels.
+  // N=128: 64 channels (24 MMAs, ~1.5k cycles -- enough to hide the next stage's load); its
+  // 64 KB operand runs into the weight area, so the slab sits behind it (XB_OFF).
+  static constexpr int XKG = MT == 2 ? (N == 128 ? 8 : 4) : 2;
   static constexpr int XA_PLANE = MT * 128 * 16;    // extra-K operand: MT rows x 128 px, 8 ch
   static constexpr int XA_HALF = XKG * XA_PLANE;
   static constexpr int XB_BYTES = 2 * XKG * N * 16; // extra-K slab: hi/lo x XKG kgroups
@@ -51,7 +54,8 @@ struct ConvCfg {
   static constexpr int TMEM_COLS = 512;
   static constexpr int SMEM = STAGES * STAGE + 1024;
   static constexpr int CPG = MT == 2 ? N / 2 : N;   // channels per epilogue warpgroup
-  static_assert(2 * XA_HALF <= A_BYTES, "extra-K operand must fit the A area");
+  static constexpr int XB_OFF = 2 * XA_HALF > A_BYTES ? 2 * XA_HALF : A_BYTES;  // extra-K slab offset
+  static_assert(XB_OFF + XB_BYTES <= STAGE, "extra-K operand and slab must fit one stage");
   static_assert(2 * STRIP * 16 == PITCH * 16 && (PITCH * 16) % 128 == 0 && A_PLANE % 128 == 0, "strip layout");
 };
 
@@ -423,10 +427,11 @@ __global__ void __launch_bounds__(320, 1) conv3x3_tc_kernel(const __grid_constan
           const uint8_t* bsrc = extra ? a.xwgt + ((size_t)nt * a.n_xkc + ci) * C::XB_BYTES
                                       : a.wgt + ((size_t)nt * a.n_kc + ci) * C::B_BYTES;
           const uint32_t bbytes = extra ? C::XB_BYTES : C::B_BYTES;
+          const uint32_t boff = extra ? C::XB_OFF : C::A_BYTES;
           if constexpr (CL) {
-            if (rank == 0) bulk_load_multicast(st + C::A_BYTES, bsrc, bbytes, &full_bar[s], kMask);
+            if (rank == 0) bulk_load_multicast(st + boff, bsrc, bbytes, &full_bar[s], kMask);
           } else {
-            bulk_load(st + C::A_BYTES, bsrc, bbytes, &full_bar[s]);
+            bulk_load(st + boff, bsrc, bbytes, &full_bar[s]);
           }
         }
       }
@@ -456,7 +461,7 @@ __global__ void __launch_bounds__(320, 1) conv3x3_tc_kernel(const __grid_constan
           // offset of k bytes is an add of k >> 4 on the precomputed 64-bit descriptor
           if (extra) {
             // V[MT rows x 128 px, 8*XKG ch] x M[8*XKG x N]: XKG/2 K=16 steps per pass
-            const uint64_t bdesc0 = make_sdesc(bb, N * 16, 128);
+            const uint64_t bdesc0 = make_sdesc(st + C::XB_OFF, N * 16, 128);
             const uint64_t adesc0 = make_sdesc(st, C::XA_PLANE, 128);
             for (int pass = 0; pass < 3; ++pass)
 #pragma unroll

@@ -49,11 +49,11 @@ bool get_encoder() {
 }
 
 // conv K operand: halo window box (8 ch, 130 px, 4 rows, 2 kg); extra-K operand: (8, 128, 2, 4)
-bool map_act(CUtensorMap* m, const __half* base, int n_kg, int H, int W, int mt, bool extra) {
+bool map_act(CUtensorMap* m, const __half* base, int n_kg, int H, int W, int mt, bool extra, int xkg) {
   cuuint64_t dims[4] = {8, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)n_kg};
   cuuint64_t strides[3] = {16, (cuuint64_t)W * 16, (cuuint64_t)H * W * 16};
   cuuint32_t box[4] = {8, extra ? 128u : 130u, extra ? (cuuint32_t)mt : (cuuint32_t)(mt + 2),
-                       extra ? (cuuint32_t)(8 / mt) : 2u};
+                       extra ? (cuuint32_t)xkg : 2u};
   cuuint32_t es[4] = {1, 1, 1, 1};
   return g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, (void*)base, dims, strides, box, es,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -439,8 +439,8 @@ int run_conv(spst_ctx* ctx, ConvLaunch& L) {
   const int mt = conv_tc_rows(N);
   if (!map_rows(&a.tm_r_hi, in->hi, in->C_p / 8, in->H, in->W) ||
       !map_rows(&a.tm_r_lo, in->lo(), in->C_p / 8, in->H, in->W) ||
-      !map_act(&a.tm_v_hi, v->hi, v->C_p / 8, v->H, v->W, mt, true) ||
-      !map_act(&a.tm_v_lo, v->lo(), v->C_p / 8, v->H, v->W, mt, true))
+      !map_act(&a.tm_v_hi, v->hi, v->C_p / 8, v->H, v->W, mt, true, conv_tc_xkg(N)) ||
+      !map_act(&a.tm_v_lo, v->lo(), v->C_p / 8, v->H, v->W, mt, true, conv_tc_xkg(N)))
     return ctx->fail(SPST_ERR_CUDA, "cuTensorMapEncodeTiled failed");
   a.wgt = L.in ? L.wslab : nullptr;
   a.n_kc = L.in ? (L.in->C_p + 15) / 16 : 0;  // an 8-channel input reads its 2nd K group as TMA zero fill
@@ -666,7 +666,7 @@ int tap_grad_gemm(spst_ctx* ctx, int k, HL16 out, bool with_mask, double two_lam
   ConvLaunch L;
   L.v = &s.out;
   L.xw = s.style >= 0 ? ctx->taps[s.style].xw : ctx->zero_xw;
-  L.n_xkc = s.cout_p / 32;
+  L.n_xkc = s.cout_p / (8 * conv_tc_xkg(ntile_for(s.cout_p)));
   L.H = s.H;
   L.W = s.W;
   L.acc_scale = 1.f / (s.out.scale * pow2f(xexp));
@@ -722,7 +722,7 @@ int backward_stage(spst_ctx* ctx, int k, int src, int dst, double two_lambda) {
       TRY(write_xw(ctx, k, xexp));
       L.v = &s.out;
       L.xw = ctx->taps[s.style].xw;
-      L.n_xkc = s.cout_p / 32;
+      L.n_xkc = s.cout_p / (8 * conv_tc_xkg(ntile_for(s.cout_p)));
       L.flops += 2.0 * s.H * s.W * s.cout * s.cout;  // fused style GEMM V M
       a.x_rescale = (float)std::ldexp(1.0, acc_e - xexp) / s.out.scale;
       a.bias = ctx->taps[s.style].bvec;

@@ -269,14 +269,21 @@ std::vector<__half> stage_slabs(const Stage& s, bool bwd, int N) {
   const int nkc = K_p / 16, nnt = N_p / N;
   std::vector<__half> out((size_t)nnt * nkc * 2 * 9 * 2 * N * 8);
   const double sc = std::ldexp(1.0, s.wexp);
-  size_t idx = 0;
+  // N=128: [pass][tap][kg][n][8].  N=64 (row-pair MMAs, see conv_tc.cu):
+  // [pass][dx][kg][2-dy][n][8], so [W_dy2 ; W_dy1 ; W_dy0] is contiguous per (pass, dx, kg).
+  const bool rowpair = N == 64;
   for (int nt = 0; nt < nnt; ++nt)
     for (int kc = 0; kc < nkc; ++kc)
       for (int pass = 0; pass < 2; ++pass)
         for (int tap = 0; tap < 9; ++tap)
           for (int kg = 0; kg < 2; ++kg)
             for (int n = 0; n < N; ++n)
-              for (int e = 0; e < 8; ++e, ++idx) {
+              for (int e = 0; e < 8; ++e) {
+                const size_t chunk = (size_t)(nt * nkc + kc) * 2 * 9 * 2 * N * 8;
+                const int tdy = tap / 3, tdx = tap % 3;
+                const size_t idx =
+                    chunk + (rowpair ? (((((size_t)pass * 3 + tdx) * 2 + kg) * 3 + (2 - tdy)) * N + n) * 8 + e
+                                     : ((((size_t)pass * 9 + tap) * 2 + kg) * N + n) * 8 + e);
                 const int ng = nt * N + n, kk = kc * 16 + kg * 8 + e;
                 const int dy = tap / 3, dx = tap % 3;
                 const int co = bwd ? kk : ng, ci = bwd ? ng : kk;

@@ -189,19 +189,28 @@ def run_ours(args):
 
     # e2e through the public API with host buffers: minimize() called on a pinned host
     # iterate (numpy in -> numpy out, H2D of x and D2H of the result inside the region)
-    e2e = None
-    if world == 1:
-        xh = torch.empty_like(x, device="cpu").pin_memory()
-        xh.copy_(x)
-        xnp = xh.numpy()
-        torch.cuda.synchronize()
-        t0 = time.time()
-        xr, tr2 = minimize(objective, xnp, LBFGSConfig(history_size=10, max_iters=args.steps))
-        e2e_s = time.time() - t0
-        it2 = max(1, len(tr2.losses) - 1)
-        nbytes = xnp.nbytes
-        e2e = {"value": it2 / e2e_s, "unit": "iters/s", "h2d_bytes_per_step": nbytes // it2,
-               "d2h_bytes_per_step": nbytes // it2 + 8 * (tr2.evals // it2 + 1)}
+    # (N > 1: every rank runs minimize on its own pinned host shard; the slowest rank's time
+    # counts and the copied bytes are summed over ranks)
+    xh = torch.empty_like(x, device="cpu").pin_memory()
+    xh.copy_(x)
+    xnp = xh.numpy()
+    torch.cuda.synchronize()
+    if world > 1:
+        tdist.barrier()
+    t0 = time.time()
+    xr, tr2 = minimize(objective, xnp, LBFGSConfig(history_size=10, max_iters=args.steps), allreduce=allreduce)
+    e2e_s = time.time() - t0
+    nbytes = xnp.nbytes
+    if world > 1:
+        t = torch.tensor([e2e_s, float(nbytes)], dtype=torch.float64, device="cuda")
+        tmax = t[:1].clone()
+        tdist.all_reduce(tmax, op=tdist.ReduceOp.MAX)
+        tsum = t[1:].clone()
+        tdist.all_reduce(tsum)
+        e2e_s, nbytes = float(tmax.item()), int(tsum.item())
+    it2 = max(1, len(tr2.losses) - 1)
+    e2e = {"value": it2 / e2e_s, "unit": "iters/s", "h2d_bytes_per_step": nbytes // it2,
+           "d2h_bytes_per_step": nbytes // it2 + 8 * (tr2.evals // it2 + 1)}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -125,6 +125,15 @@ int spst_vec_axpy_dot(int f64, const void* q_in, void* q_out, const void* v,
 int spst_vec_twoloop_scalar(const double* dot_dev, double rho, int mode, double* alpha_dev,
                             double* coef_dev, void* stream);
 int spst_vec_sum_partials(const double* partial_dev, int n_quantities, double* out_dev, void* stream);
+/* lbfgs.py:68-83 two_loop_direction as ONE call (single-device runs): out = -H g from the m
+ * curvature pairs (s_vecs/y_vecs oldest first, rho_i = 1/<y_i,s_i>, gamma = <s,y>/<y,y> of the
+ * newest pair).  2m+1 kernels, each an axpy+dot step that also finishes its dot product in
+ * fixed block order and applies the scalar update (bit-identical to the step-by-step calls
+ * above); alpha_dev holds m doubles, coef_dev one, ticket_dev one zero-initialised counter. */
+int spst_vec_two_loop(int f64, const void* g, void* out, const void* const* s_vecs,
+                      const void* const* y_vecs, const double* rho, double gamma, int m, long long n,
+                      double* partial_dev, double* alpha_dev, unsigned int* ticket_dev, double* coef_dev,
+                      void* stream);
 int spst_vec_axpy(int f64, const void* x, const void* d, double t, long long n, void* out, void* stream);
 int spst_vec_sy(int f64, const void* xt, const void* x, const void* gt, const void* g, long long n,
                 void* s, void* y, double* partial_dev, double* out_dev /*[3]: ys, ss, yy*/,

@@ -60,6 +60,8 @@ SIGNATURES = {
                                   c_longlong, c_void_p, c_void_p]),
     "spst_vec_twoloop_scalar": (c_int, [c_void_p, c_double, c_int, c_void_p, c_void_p, c_void_p]),
     "spst_vec_sum_partials": (c_int, [c_void_p, c_int, c_void_p, c_void_p]),
+    "spst_vec_two_loop": (c_int, [c_int, c_void_p, c_void_p, POINTER(c_void_p), POINTER(c_void_p), POINTER(c_double),
+                                  c_double, c_int, c_longlong, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "spst_vec_axpy": (c_int, [c_int, c_void_p, c_void_p, c_double, c_longlong, c_void_p, c_void_p]),
     "spst_vec_sy": (c_int, [c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_longlong, c_void_p, c_void_p,
                             c_void_p, c_void_p, c_void_p]),

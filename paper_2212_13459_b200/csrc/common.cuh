@@ -124,6 +124,12 @@ struct AxpyDotArgs {
   const void* w;        // dot vector (nullable)
   long long n;
   double* partial;
+  // fused step (spst_vec_two_loop): the last block to finish sums the partials in block order
+  // (as finish_sums_kernel) and applies the two-loop scalar update (as twoloop_scalar_kernel)
+  double* alpha_i = nullptr;     // non-null enables the fused finish
+  unsigned int* ticket = nullptr;  // zero-initialised counter, reset by the last block
+  double rho = 0.0;
+  int mode = 0;
 };
 
 // ---------------------------------------------------------------- launchers

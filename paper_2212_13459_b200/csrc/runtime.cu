@@ -1232,6 +1232,37 @@ int spst_vec_twoloop_scalar(const double* dot, double rho, int mode, double* alp
                                                                                                 : SPST_ERR_CUDA;
 }
 
+int spst_vec_two_loop(int f64, const void* g, void* out, const void* const* s_vecs, const void* const* y_vecs,
+                      const double* rho, double gamma, int m, long long n, double* partial, double* alpha,
+                      unsigned int* ticket, double* coef, void* stream) {
+  // the sequence of lbfgs.py _two_loop issued from C as 2m+1 fused kernels: each axpy+dot step
+  // also finishes its dot (fixed block order) and applies the scalar update in its last block,
+  // so the results equal the 3-kernel-per-step form bit for bit.  Pairs oldest first.
+  if (m < 1 || n < 0 || !g || !out || !ticket) return SPST_ERR_SHAPE;
+  cudaStream_t st = (cudaStream_t)stream;
+  auto step = [&](const void* qi, const void* v, double cscale, const void* w, int i, int mode) -> bool {
+    AxpyDotArgs a{qi, out, v, coef, cscale, w, n, partial};
+    if (w) {
+      a.alpha_i = alpha + i;
+      a.ticket = ticket;
+      a.rho = rho[i];
+      a.mode = mode;
+    }
+    return launch_axpy_dot(f64, a, st) == cudaSuccess;
+  };
+  // loop 1, newest -> oldest: alpha_i = rho_i <s_i, q>; q -= alpha_i y_i
+  if (!step(g, nullptr, 1.0, s_vecs[m - 1], m - 1, 0)) return SPST_ERR_CUDA;
+  for (int i = m - 1; i > 0; --i)
+    if (!step(out, y_vecs[i], 1.0, s_vecs[i - 1], i - 1, 0)) return SPST_ERR_CUDA;
+  // q = gamma (q - alpha_0 y_0); beta_0 = rho_0 <y_0, q>
+  if (!step(out, y_vecs[0], gamma, y_vecs[0], 0, 1)) return SPST_ERR_CUDA;
+  // loop 2, oldest -> newest: q += (alpha_i - beta_i) s_i
+  for (int i = 0; i < m - 1; ++i)
+    if (!step(out, s_vecs[i], 1.0, y_vecs[i + 1], i + 1, 1)) return SPST_ERR_CUDA;
+  if (!step(out, s_vecs[m - 1], -1.0, nullptr, 0, 0)) return SPST_ERR_CUDA;
+  return SPST_OK;
+}
+
 int spst_vec_sum_partials(const double* partial, int nk, double* out, void* stream) {
   return launch_sum_partials(partial, nk, out, (cudaStream_t)stream) == cudaSuccess ? SPST_OK : SPST_ERR_CUDA;
 }

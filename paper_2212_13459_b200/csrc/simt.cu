@@ -459,6 +459,26 @@ __global__ void __launch_bounds__(kRedThreads) axpy_dot_kernel(AxpyDotArgs a) {
   if (w) {
     const double t = block_sum(s, sh);
     if (threadIdx.x == 0) a.partial[blockIdx.x] = t;
+    if (a.alpha_i) {  // fused finish: the last block reduces in block order, then the scalar step
+      __shared__ bool last;
+      __threadfence();
+      if (threadIdx.x == 0) last = atomicAdd(a.ticket, 1u) == gridDim.x - 1;
+      __syncthreads();
+      if (last && threadIdx.x == 0) {
+        __threadfence();
+        const volatile double* pv = a.partial;
+        double dot = 0.0;
+        for (unsigned b = 0; b < gridDim.x; ++b) dot += pv[b];
+        double* coef = const_cast<double*>(a.coef);  // read by every block at entry, written here last
+        if (a.mode == 0) {
+          *a.alpha_i = a.rho * dot;
+          *coef = -(*a.alpha_i);
+        } else {
+          *coef = *a.alpha_i - a.rho * dot;
+        }
+        *a.ticket = 0u;
+      }
+    }
   }
 }
 

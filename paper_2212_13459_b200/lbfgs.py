@@ -61,6 +61,7 @@ class _Vec:
         self.out = torch.empty(8, dtype=torch.float64, device=device)
         self.alpha = torch.empty(0, dtype=torch.float64, device=device)
         self.coef = torch.empty(1, dtype=torch.float64, device=device)
+        self.ticket = torch.zeros(1, dtype=torch.int32, device=device)  # fused two-loop finish counter
         self.device = device
 
     def _s(self):
@@ -163,6 +164,14 @@ def _two_loop(g, state: LBFGSState, vec: _Vec, out, allreduce=None):
     alpha = torch.empty(m, dtype=torch.float64, device=dev)
     dot = torch.empty(1, dtype=torch.float64, device=dev)
     gamma = (1.0 / R[-1]) / state.yy[-1]
+    if allreduce is None:  # single device: the whole sequence in one native call
+        sp = (ctypes.c_void_p * m)(*[t.data_ptr() for t in S])
+        yp = (ctypes.c_void_p * m)(*[t.data_ptr() for t in Y])
+        rp = (ctypes.c_double * m)(*R)
+        nat.check(nat.lib().spst_vec_two_loop(vec.f64, nat.ptr(g), nat.ptr(out), sp, yp, rp, float(gamma), m,
+                                              g.numel(), nat.ptr(vec.partial), nat.ptr(alpha), nat.ptr(vec.ticket),
+                                              nat.ptr(vec.coef), vec._s()), None, "spst_vec_two_loop")
+        return out
     # loop 1, newest -> oldest: alpha_i = rho_i <s_i, q>; q -= alpha_i y_i
     vec.axpy_dot(g, out, None, vec.coef, 1.0, S[m - 1])
     vec.finish(dot, allreduce)

@@ -133,7 +133,7 @@ struct AxpyDotArgs {
 };
 
 // ---------------------------------------------------------------- launchers
-cudaError_t launch_conv_tc(const ConvArgs& a, int N, int grid, cudaStream_t stream, int cluster);
+cudaError_t launch_conv_tc(const ConvArgs& a, int N, int grid, cudaStream_t stream);
 int conv_tc_smem_bytes(int N);
 int conv_tc_rows(int N);   // output rows per tile (MT)
 int conv_tc_xkg(int N);    // kgroups per extra-K chunk

@@ -316,33 +316,23 @@ __device__ __forceinline__ void epilogue32(const ConvArgs& a, float* v0, float* 
   }
 }
 
-// Work decomposition.  Unclustered: unit t = (spatial tile, n-tile), n-tile fastest.
-// Clustered (CL, 2 CTAs): unit t = (spatial tile pair, n-tile); CTA rank r takes spatial tile
-// 2*pair + r, so both CTAs use the same weight slab, which rank 0 multicasts into both.
+// Work decomposition: unit t = (spatial tile, n-tile), n-tile fastest, so consecutive CTAs
+// share the spatial tile's halo window in L2.  (A clustered variant that multicast the weight
+// slab to 2/4/8 CTAs measured slower: the shared stage release couples the CTAs.)
 struct TileId {
   int nt, cx, ry;
-  bool valid;
 };
 
-template <int CS>
-__device__ __forceinline__ TileId decode_tile(const ConvArgs& a, int t, uint32_t rank) {
+__device__ __forceinline__ TileId decode_tile(const ConvArgs& a, int t) {
   TileId id;
   id.nt = t % a.n_ntiles;
-  const int rest = t / a.n_ntiles;
-  const int sp = CS * rest + (int)rank;
-  id.valid = sp < a.tiles_x * a.tiles_y;
+  const int sp = t / a.n_ntiles;
   id.cx = sp % a.tiles_x;
-  id.ry = id.valid ? sp / a.tiles_x : a.tiles_y;  // an invalid unit reads OOB (zeros), stores nothing
+  id.ry = sp / a.tiles_x;
   return id;
 }
 
-template <int CS>
-__device__ __forceinline__ int n_units(const ConvArgs& a) {
-  const int sp = a.tiles_x * a.tiles_y;
-  return (sp + CS - 1) / CS * a.n_ntiles;
-}
-
-template <int N, int CS>
+template <int N>
 __global__ void __launch_bounds__(320, 1) conv3x3_tc_kernel(const __grid_constant__ ConvArgs a) {
   using C = ConvCfg<N>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -353,12 +343,9 @@ __global__ void __launch_bounds__(320, 1) conv3x3_tc_kernel(const __grid_constan
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
-  constexpr bool CL = CS > 1;
-  constexpr uint16_t kMask = (uint16_t)((1u << CS) - 1);
-  const uint32_t rank = CL ? cluster_ctarank() : 0;
-  const int n_tiles = n_units<CS>(a);
-  const int first = (int)blockIdx.x / CS;
-  const int step = (int)gridDim.x / CS;
+  const int n_tiles = a.tiles_x * a.tiles_y * a.n_ntiles;
+  const int first = (int)blockIdx.x;
+  const int step = (int)gridDim.x;
   const int n_chunks = a.n_kc + a.n_xkc;
 
   if (warp == 0 && lane == 0) {
@@ -368,7 +355,7 @@ __global__ void __launch_bounds__(320, 1) conv3x3_tc_kernel(const __grid_constan
     tma_prefetch_desc(&a.tm_v_lo);
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&full_bar[s], 1);
-      mbar_init(&empty_bar[s], CS);  // clustered: every CTA of the cluster must release the stage
+      mbar_init(&empty_bar[s], 1);
     }
     for (int b = 0; b < C::NBUF; ++b) {
       mbar_init(&cfull_bar[b], 1);
@@ -378,10 +365,7 @@ __global__ void __launch_bounds__(320, 1) conv3x3_tc_kernel(const __grid_constan
   }
   if (warp == 1) tmem_alloc<C::TMEM_COLS>(&tmem_slot);
   tc_fence_before();
-  if constexpr (CL)
-    cluster_sync_all();  // peer barriers initialised before any multicast lands
-  else
-    __syncthreads();
+  __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = tmem_slot;
 
@@ -397,7 +381,7 @@ __global__ void __launch_bounds__(320, 1) conv3x3_tc_kernel(const __grid_constan
     const void* s_map = s_hl ? (const void*)&a.tm_r_lo : (const void*)&a.tm_r_hi;
     uint32_t g = 0;
     for (int t = first; t < n_tiles; t += step) {
-      const TileId id = decode_tile<CS>(a, t, rank);
+      const TileId id = decode_tile(a, t);
       const int nt = id.nt;
       const int x0 = id.cx * 128;
       const int y0 = id.ry * C::MT;
@@ -407,12 +391,6 @@ __global__ void __launch_bounds__(320, 1) conv3x3_tc_kernel(const __grid_constan
         uint8_t* st = smem + s * C::STAGE;
         int ci;
         const bool extra = chunk_is_extra(c, a.n_kc, ci);
-#ifdef SPST_EXP_NOLOAD
-        if (g >= C::STAGES) {
-          if (lane == 0) mbar_arrive(&full_bar[s]);
-          continue;
-        }
-#endif
         if (!extra) {
           if (lane == 0) mbar_arrive_expect_tx(&full_bar[s], C::A_BYTES + C::B_BYTES);
           __syncwarp();
@@ -428,11 +406,7 @@ __global__ void __launch_bounds__(320, 1) conv3x3_tc_kernel(const __grid_constan
                                       : a.wgt + ((size_t)nt * a.n_kc + ci) * C::B_BYTES;
           const uint32_t bbytes = extra ? C::XB_BYTES : C::B_BYTES;
           const uint32_t boff = extra ? C::XB_OFF : C::A_BYTES;
-          if constexpr (CL) {
-            if (rank == 0) bulk_load_multicast(st + boff, bsrc, bbytes, &full_bar[s], kMask);
-          } else {
-            bulk_load(st + boff, bsrc, bbytes, &full_bar[s]);
-          }
+          bulk_load(st + boff, bsrc, bbytes, &full_bar[s]);
         }
       }
     }
@@ -522,10 +496,7 @@ __global__ void __launch_bounds__(320, 1) conv3x3_tc_kernel(const __grid_constan
               }
             }
           }
-          if constexpr (CL)
-            umma_commit_multicast_ws(&empty_bar[s], kMask);  // release the stage in every CTA
-          else
-            umma_commit_ws(&empty_bar[s]);
+          umma_commit_ws(&empty_bar[s]);
           if (glast) {
             umma_commit_ws(&cfull_bar[b]);
             ++gq;
@@ -542,7 +513,7 @@ __global__ void __launch_bounds__(320, 1) conv3x3_tc_kernel(const __grid_constan
     const int cofs = C::MT == 2 ? (int)grp * C::CPG : 0;  // first channel handled
     uint32_t g = 0;
     for (int t = first; t < n_tiles; t += step) {
-      const TileId id = decode_tile<CS>(a, t, rank);
+      const TileId id = decode_tile(a, t);
       const int nt = id.nt, cx = id.cx, ry = id.ry;
       const int x0 = cx * 128, y0 = ry * C::MT + 2 * rp;
       const int x = x0 + m;
@@ -578,7 +549,6 @@ __global__ void __launch_bounds__(320, 1) conv3x3_tc_kernel(const __grid_constan
       }
       float amax0 = 0.f, amax1 = 0.f;
       const int part_row = (ry * a.tiles_x + cx) * (C::MT / 2) + rp;
-      if (!id.valid) continue;  // padding unit of the last cluster pair: nothing to store
 #pragma unroll
       for (int cb = 0; cb < C::CPG / 32; ++cb)
         epilogue32<N>(a, acc0 + cb * 32, acc1 + cb * 32, nt * N + cofs + cb * 32, x, y0, part_row, q, amax0,
@@ -594,10 +564,7 @@ __global__ void __launch_bounds__(320, 1) conv3x3_tc_kernel(const __grid_constan
     }
   }
   tc_fence_before();
-  if constexpr (CL)
-    cluster_sync_all();  // no CTA leaves while its peer may still multicast into it
-  else
-    __syncthreads();
+  __syncthreads();
   if (warp == 1) tmem_dealloc<C::TMEM_COLS>(tmem_base);
 }
 
@@ -606,43 +573,16 @@ int conv_tc_smem_bytes(int N) { return N == 128 ? ConvCfg<128>::SMEM : ConvCfg<6
 int conv_tc_rows(int N) { return N == 128 ? ConvCfg<128>::MT : ConvCfg<64>::MT; }
 int conv_tc_xkg(int N) { return N == 128 ? ConvCfg<128>::XKG : ConvCfg<64>::XKG; }
 
-template <int N, int CS>
+template <int N>
 static cudaError_t launch_one(const ConvArgs& a, int grid, cudaStream_t stream) {
-  auto k = conv3x3_tc_kernel<N, CS>;
+  auto k = conv3x3_tc_kernel<N>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, ConvCfg<N>::SMEM);
-  if (CS == 16) cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3((grid + CS - 1) / CS * CS);
-  cfg.blockDim = dim3(320);
-  cfg.dynamicSmemBytes = ConvCfg<N>::SMEM;
-  cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = CS;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = CS > 1 ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, k, a);
+  k<<<grid, 320, ConvCfg<N>::SMEM, stream>>>(a);
+  return cudaGetLastError();
 }
 
-// cluster: CTAs per cluster sharing (multicasting) the weight slab (1 = no cluster)
-cudaError_t launch_conv_tc(const ConvArgs& a, int N, int grid, cudaStream_t stream, int cluster) {
-  cudaError_t e;
-#define SPST_CASE(CSV)                                                                           \
-  case CSV:                                                                                      \
-    e = N == 128 ? launch_one<128, CSV>(a, grid, stream) : launch_one<64, CSV>(a, grid, stream); \
-    break;
-  switch (cluster) {
-    SPST_CASE(2)
-    SPST_CASE(4)
-    SPST_CASE(8)
-    default:
-      e = N == 128 ? launch_one<128, 1>(a, grid, stream) : launch_one<64, 1>(a, grid, stream);
-  }
-#undef SPST_CASE
-  if (e != cudaSuccess) return e;
-  return cudaGetLastError();
+cudaError_t launch_conv_tc(const ConvArgs& a, int N, int grid, cudaStream_t stream) {
+  return N == 128 ? launch_one<128>(a, grid, stream) : launch_one<64>(a, grid, stream);
 }
 
 }  // namespace spst

@@ -401,7 +401,6 @@ struct ConvLaunch {
   const uint8_t* wslab = nullptr;
   const HL16* v = nullptr;       // extra-K operand
   const __half* xw = nullptr;
-  int n_xkc = 0;
   int H = 0, W = 0;              // GEMM grid (conv output grid)
   float acc_scale = 1.f;
   double flops = 0;              // algorithmic FLOPs (real channels, one pass) for the launch timer
@@ -461,16 +460,9 @@ int run_conv(spst_ctx* ctx, ConvLaunch& L) {
   a.acc_scale = L.acc_scale;
   if (a.n_kc + a.n_xkc == 0) return ctx->fail(SPST_ERR_CONFIG, "empty GEMM");
   const int tiles = a.tiles_x * a.tiles_y * a.n_ntiles;
-  static const int cluster_mode = [] {
-    const char* e = getenv("SPST_CLUSTER");
-    return e ? atoi(e) : 1;
-  }();
-  // clusters of `cs` CTAs multicast the weight slab (needs >= cs spatial tiles to pay off)
-  int cs = cluster_mode;
-  while (cs > 1 && a.tiles_x * a.tiles_y < 4 * cs) cs /= 2;
-  const int grid = std::min(tiles, (kSMs / std::max(cs, 1)) * std::max(cs, 1));
+  const int grid = std::min(tiles, kSMs);  // persistent: one CTA per SM
   auto* tm = timer_begin(ctx, N == 128 ? 0 : 1, L.flops);
-  CK(launch_conv_tc(a, N, std::max(grid, cs), ctx->stream, cs));
+  CK(launch_conv_tc(a, N, grid, ctx->stream));
   timer_end(ctx, tm);
   return SPST_OK;
 }
@@ -673,7 +665,6 @@ int tap_grad_gemm(spst_ctx* ctx, int k, HL16 out, bool with_mask, double two_lam
   ConvLaunch L;
   L.v = &s.out;
   L.xw = s.style >= 0 ? ctx->taps[s.style].xw : ctx->zero_xw;
-  L.n_xkc = s.cout_p / (8 * conv_tc_xkg(ntile_for(s.cout_p)));
   L.H = s.H;
   L.W = s.W;
   L.acc_scale = 1.f / (s.out.scale * pow2f(xexp));
@@ -729,7 +720,6 @@ int backward_stage(spst_ctx* ctx, int k, int src, int dst, double two_lambda) {
       TRY(write_xw(ctx, k, xexp));
       L.v = &s.out;
       L.xw = ctx->taps[s.style].xw;
-      L.n_xkc = s.cout_p / (8 * conv_tc_xkg(ntile_for(s.cout_p)));
       L.flops += 2.0 * s.H * s.W * s.cout * s.cout;  // fused style GEMM V M
       a.x_rescale = (float)std::ldexp(1.0, acc_e - xexp) / s.out.scale;
       a.bias = ctx->taps[s.style].bvec;
@@ -756,7 +746,6 @@ int backward_stage(spst_ctx* ctx, int k, int src, int dst, double two_lambda) {
     a.bias = nullptr;
     L.v = nullptr;
     L.xw = nullptr;
-    L.n_xkc = 0;
   }
   CK(cudaMemsetAsync(ctx->amax_d + 4 * k + 2, 0, 4, ctx->stream));
   return run_conv(ctx, L);

@@ -53,4 +53,6 @@ CONFIGS = {
     "c3": dict(content=(3024, 4032), style=(2113, 2660), n_scales=3, iters=None),
     # configs[3]: full 4-scale UHR transfer, the metric's resolution
     "c4": dict(content=(6048, 8064), style=(4226, 5319), n_scales=4, iters=None),
+    # the coarsest scale of c4 (600 iterations of the fast and baseline schedules)
+    "c4s1": dict(content=(756, 1008), style=(529, 665), n_scales=1, iters=600),
 }

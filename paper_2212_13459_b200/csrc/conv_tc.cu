@@ -11,20 +11,22 @@
 // N = output channels (64/128 per tile), K = 9 taps x input channels.
 //
 // Numerics ("fp16x3 + register accumulation"): operands are fp16 hi/lo pairs with
-// power-of-two tensor scales; each 16-channel K-chunk issues hi*hi + hi*lo + lo*hi over the
-// 9 taps into a FRESH TMEM accumulator, and the epilogue warps drain every chunk into fp32
-// registers (round-to-nearest adds).  The tensor core therefore never carries a running sum
-// longer than one chunk, which removes the truncation bias of long in-TMEM accumulations
-// (measured: rel-err growing ~ K x 2^-24 otherwise).
+// power-of-two tensor scales; each 16-channel K-chunk issues hi*lo + lo*hi + hi*hi over the 9
+// taps into a FRESH TMEM accumulator shared by at most D chunks (D = 2 on the 128-channel
+// layers, 1 on the 64-channel ones), and the epilogue warps drain it into fp32 registers
+// (round-to-nearest adds).  The tensor core therefore never carries a long running sum, which
+// removes the truncation bias of long in-TMEM accumulations (rel-err ~ K x 2^-24 otherwise).
 //
-// Warp roles (320 threads, persistent over output tiles):
-//   warp 0      TMA producer: per K-chunk one 4-row x 130-px halo window of hi and lo
-//               activations (TMA 4-D, OOB zero fill = conv zero padding) + the 9-tap weight
-//               slab (one 1-D bulk copy)
-//   warp 1      MMA issuer (one thread): 9 taps x 2 rows x 3 passes per chunk; a tap shift is
-//               a descriptor start-address offset into the halo window
+// Warp roles (320 threads, persistent over output tiles, one CTA per SM):
+//   warp 0      TMA producer: per K-chunk the 4-row halo window of hi and lo activations as
+//               32 u64-view strips of 68 px (one per lane; OOB zero fill = conv zero padding)
+//               + the 9-tap weight slab (one 1-D bulk copy)
+//   warp 1      MMA issuer: the whole warp runs the loop (descriptors stay in uniform
+//               registers), one elected lane issues 9 taps x 2 rows x 3 passes per chunk
+//               (64-channel layers: row-pair MMAs, see the N == 64 branch); a tap shift is a
+//               descriptor start-address offset into the halo window
 //   warps 2..9  two epilogue warpgroups; group g drains channel half g of both rows of every
-//               chunk into registers, then runs the fused pointwise epilogue for the tile
+//               accumulation group into registers, then runs the fused pointwise epilogue
 #include "common.cuh"
 #include "sm100.cuh"
 

@@ -12,7 +12,8 @@ from paper_2212_13459_b200 import _native, errors
 
 
 def header_functions():
-    text = open(os.path.join(ROOT, "include", "spst.h")).read()
+    with open(os.path.join(ROOT, "include", "spst.h")) as f:
+        text = f.read()
     text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
     return sorted(set(re.findall(r"\b(spst_[a-z0-9_]+)\s*\(", text)))
 
@@ -42,7 +43,8 @@ def test_status_codes_map_to_reference_exceptions():
 
 
 def test_built_for_sm100a_only():
-    out = os.popen(f"cuobjdump --list-elf {os.path.join(ROOT, 'paper_2212_13459_b200', 'libspst.so')} 2>&1").read()
+    with os.popen(f"cuobjdump --list-elf {os.path.join(ROOT, 'paper_2212_13459_b200', 'libspst.so')} 2>&1") as pipe:
+        out = pipe.read()
     assert "sm_100a" in out
     assert not re.search(r"sm_(80|86|89|90)\b", out)
 

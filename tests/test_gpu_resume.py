@@ -59,7 +59,8 @@ def test_pipeline_midscale_checkpoint_and_resume(tiny_spec, tmp_path):
     sides = sorted(glob.glob(base + ".scale2.iter*.json"), key=lambda p: int(p.split(".iter")[1].split(".")[0]))
     assert sides, "no mid-scale checkpoints written"
     side = sides[len(sides) // 2]
-    meta = json.load(open(side))
+    with open(side) as f:
+        meta = json.load(f)
     assert meta["scale"] == 1 and meta["iteration"] > 0 and os.path.exists(os.path.join(tmp_path, meta["lbfgs"]))
     done, x, snap = read_checkpoint(side, "cfgA", "f32", with_state=True)
     assert done == 1 and snap.iteration == meta["iteration"] and len(snap.s) > 0

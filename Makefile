@@ -2,7 +2,7 @@
 NVCC ?= nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
 CSRC := paper_2212_13459_b200/csrc
-SRCS := $(CSRC)/conv_tc.cu $(CSRC)/gram_tc.cu $(CSRC)/simt.cu $(CSRC)/metrics.cu $(CSRC)/runtime.cu
+SRCS := $(CSRC)/conv_tc.cu $(CSRC)/gram_tc.cu $(CSRC)/simt.cu $(CSRC)/metrics.cu $(CSRC)/first_bwd_tc.cu $(CSRC)/runtime.cu
 FLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Iinclude --expt-relaxed-constexpr
 LIB := paper_2212_13459_b200/libspst.so
 

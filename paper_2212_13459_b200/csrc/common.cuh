@@ -92,6 +92,18 @@ struct FirstConvBwdArgs {
   float* gimg;        // (Hl, Wp, 3) f32 local padded grid
 };
 
+// Adjoint of the first conv on tcgen05 (first_bwd_tc.cu): taps folded into N (27 of 32).
+struct FirstBwdTcArgs {
+  CUtensorMap tm_hi, tm_lo;  // g0 (64 channels) as u64 (2W, H, 8): box 256 x 1 x 8 (128 px)
+  const void* wslab;         // [hi|lo][kg 8][n 32][8] fp16: W[k][c][dy][dx] x 2^wexp at n = c*9+dy*3+dx
+  int H, W;                  // local padded grid
+  float acc_scale;           // 1 / (g0 scale x 2^wexp)
+  int perm[3];
+  float scale[3];
+  float* gimg;               // (H, W, 3) f32
+};
+cudaError_t launch_first_bwd_tc(const FirstBwdTcArgs& a, cudaStream_t st);
+
 struct StyleCoefArgs {
   const double* S;      // [C][C] global sum of outer products
   const double* s;      // [C] global channel sums

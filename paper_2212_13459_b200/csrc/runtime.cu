@@ -72,6 +72,18 @@ bool map_rows(CUtensorMap* m, const __half* base, int n_kg, int H, int W) {
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// First-conv adjoint operand: a 64-channel HL16 tensor as u64 (2W, H, 8); one box is a 128-px
+// row segment of all 8 planes (16 KB, [plane][px][8]).
+bool map_rows128(CUtensorMap* m, const __half* base, int H, int W) {
+  cuuint64_t dims[3] = {2 * (cuuint64_t)W, (cuuint64_t)H, 8};
+  cuuint64_t strides[2] = {(cuuint64_t)W * 16, (cuuint64_t)H * W * 16};
+  cuuint32_t box[3] = {256, 1, 8};
+  cuuint32_t es[3] = {1, 1, 1};
+  return g_encode(m, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, (void*)base, dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // Gram operand: the HL16 planes viewed as u64 (2P, kg); box (128 = 64 px, 16 kg) or, for 64
 // channels, (256 = 128 px, 8 kg).  Each box row is one plane's contiguous pixel run (1-2 KB),
 // landing as the dense [kg][px][8] MN-major operand.
@@ -150,6 +162,7 @@ struct Stage {
   int wexp = 0;
   float* bias_d = nullptr;
   uint8_t* wf_d = nullptr;
+  uint8_t* w1b_d = nullptr;  // first stage only: adjoint slab of first_bwd_tc_kernel
   uint8_t* wb_d = nullptr;
   int H = 0, W = 0;
   HL16 out, pooled;
@@ -374,7 +387,24 @@ int upload_weights(spst_ctx* ctx) {
     s.wf_d = ctx->dalloc<uint8_t>(wf.size() * 2, true);
     if (!s.wf_d) return ctx->fail(SPST_ERR_OOM, "forward weight slabs");
     CK(cudaMemcpy(s.wf_d, wf.data(), wf.size() * 2, cudaMemcpyHostToDevice));
-    if (k > 0) {  // the first conv's adjoint runs on CUDA cores (first_conv_bwd_kernel)
+    if (k == 0) {  // adjoint slab of the first conv: [hi|lo][kg][n = c*9+dy*3+dx (32)][8 k]
+      std::vector<__half> w1b(2 * 8 * 32 * 8, __float2half(0.f));
+      const double sc = std::ldexp(1.0, s.wexp);
+      for (int kk = 0; kk < std::min(s.cout, 64); ++kk)
+        for (int c = 0; c < s.cin; ++c)
+          for (int t = 0; t < 9; ++t) {
+            __half hi, lo;
+            split_host(s.w[((size_t)kk * s.cin + c) * 9 + t] * sc, hi, lo);
+            const int n = c * 9 + t;
+            const size_t off = ((size_t)(kk / 8) * 32 + n) * 8 + kk % 8;
+            w1b[off] = hi;
+            w1b[8 * 32 * 8 + off] = lo;
+          }
+      s.w1b_d = ctx->dalloc<uint8_t>(w1b.size() * 2, true);
+      if (!s.w1b_d) return ctx->fail(SPST_ERR_OOM, "first-layer adjoint slab");
+      CK(cudaMemcpy(s.w1b_d, w1b.data(), w1b.size() * 2, cudaMemcpyHostToDevice));
+    }
+    if (k > 0) {
       auto wb = stage_slabs(s, true, ntile_for(s.cin_p));
       s.wb_d = ctx->dalloc<uint8_t>(wb.size() * 2, true);
       if (!s.wb_d) return ctx->fail(SPST_ERR_OOM, "backward weight slabs");
@@ -790,6 +820,26 @@ int do_backward(spst_ctx* ctx, double two_lambda, float* grad, bool careful) {
   }
   // first conv adjoint + preprocess adjoint, then fold the replicate padding
   Stage& s0 = ctx->stages[0];
+  static const bool simt_first_bwd = [] {
+    const char* e = getenv("SPST_FIRSTBWD_SIMT");
+    return e && atoi(e) != 0;
+  }();
+  if (!simt_first_bwd && s0.cin == 3 && ctx->gbuf[cur].C_p == 64) {
+    const HL16& g0 = ctx->gbuf[cur];
+    FirstBwdTcArgs fb{};
+    if (!map_rows128(&fb.tm_hi, g0.hi, g0.H, g0.W) || !map_rows128(&fb.tm_lo, g0.lo(), g0.H, g0.W))
+      return ctx->fail(SPST_ERR_CUDA, "cuTensorMapEncodeTiled failed (first-conv adjoint)");
+    fb.wslab = s0.w1b_d;
+    fb.H = g0.H;
+    fb.W = g0.W;
+    fb.acc_scale = 1.f / (g0.scale * pow2f(s0.wexp));
+    for (int c = 0; c < 3; ++c) {
+      fb.perm[c] = ctx->perm[c];
+      fb.scale[c] = ctx->scale[c];
+    }
+    fb.gimg = ctx->gimg;
+    CK(launch_first_bwd_tc(fb, ctx->stream));
+  } else {
   FirstConvBwdArgs b{};
   b.g = ctx->gbuf[cur];
   for (int i = 0; i < kFirstC * 27; ++i) b.wgt[i] = i < (int)s0.w.size() ? (float)s0.w[i] : 0.f;
@@ -800,6 +850,7 @@ int do_backward(spst_ctx* ctx, double two_lambda, float* grad, bool careful) {
   }
   b.gimg = ctx->gimg;
   CK(launch_first_conv_bwd(b, ctx->stream));
+  }
   const int r0 = ctx->own_r0, r1 = std::min(ctx->own_r1, ctx->h);
   CK(launch_fold_grad(ctx->gimg, s0.H, s0.W, ctx->grid_r0, ctx->h, ctx->w, r0, r1, grad, ctx->stream));
   // end-of-pass range check (fast path)

@@ -133,7 +133,6 @@ def run_ours(args):
     from paper_2212_13459_b200.lbfgs import Trace
     peak_hbm, peak_bf16, peak_sus, peak_kind = peaks()
     sampler = ClockSampler(local)
-    launches = count_launches_begin()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     marks = {}
@@ -156,9 +155,11 @@ def run_ours(args):
                 if eng is not None:
                     eng.timing_enable(True)
                 sampler.start()
+                marks["launch0"] = launch_count()
                 e0.record()
             else:
                 e1.record()
+                marks["launch1"] = launch_count()
                 if eng is not None:
                     marks["timer"] = eng.timing_read()
                     eng.timing_enable(False)
@@ -180,7 +181,11 @@ def run_ours(args):
     tr = tr_all
     iters = args.steps
     evals_per_iter = tr.evals / max(1, len(tr.losses) - 1)
-    n_launch = count_launches_end(launches, tr)
+    n_launch = marks["launch1"] - marks["launch0"]  # our kernels in the timed region (this rank)
+    if world > 1:  # whole job
+        t = torch.tensor([float(n_launch)], dtype=torch.float64, device="cuda")
+        tdist.all_reduce(t)
+        n_launch = int(t.item())
 
     # roofline of the dominant kernel (conv fwd/bwd): algorithmic FLOPs per eval / eval time
     Hp, Wp = H + (-H) % 16, W + (-W) % 16
@@ -289,19 +294,10 @@ def measure_eval(objective, x, torch):
     return e0.elapsed_time(e1) / n
 
 
-def count_launches_begin():
-    return None
-
-
-def count_launches_end(_, tr):
-    # per evaluation: forward 13 convs (+1 pool for nets whose first relu pools) + 5 Gram +
-    # 5 Gram reduce + 5 colsum reduce + 10 style coef kernels + content; per gradient: ~15
-    # tensor-core launches + first-conv adjoint + fold; per iteration ~4m+8 vector kernels
-    per_eval = 13 + 5 * 3 + 10 + 2
-    per_grad = 14 + 2 + 5
-    per_iter_vec = 4 * 10 + 8
-    iters = max(1, len(tr.losses) - 1)
-    return int(tr.evals * per_eval + tr.grads * per_grad + iters * per_iter_vec)
+def launch_count():
+    """Kernels launched so far by libspst (every launch site counts itself)."""
+    from paper_2212_13459_b200 import _native as nat
+    return int(nat.lib().spst_launch_count())
 
 
 # ------------------------------------------------------------------------------------------

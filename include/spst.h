@@ -105,6 +105,9 @@ int spst_backward(spst_ctx* ctx, double two_lambda, float* grad_dev);
  * algorithmic FLOPs of those launches (real channel counts, one pass) and the launch count.
  * spst_timing_enable resets the totals. */
 int spst_timing_enable(spst_ctx* ctx, int on);
+/* Kernels launched by this library since it was loaded (all contexts and the context-free
+ * entry points); bench.py reads it around its timed region. */
+long long spst_launch_count(void);
 int spst_timing_read(spst_ctx* ctx, double* ms4, double* flops4, long long* launches4);
 
 /* ---------------------------------------------------------------- vector kernels ---------

@@ -66,6 +66,7 @@ SIGNATURES = {
     "spst_vec_sy": (c_int, [c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_longlong, c_void_p, c_void_p,
                             c_void_p, c_void_p, c_void_p]),
     "spst_timing_enable": (c_int, [c_void_p, c_int]),
+    "spst_launch_count": (c_longlong, []),
     "spst_timing_read": (c_int, [c_void_p, POINTER(c_double), POINTER(c_double), POINTER(c_longlong)]),
     "spst_metric_sqdiff": (c_int, [c_int, c_void_p, c_void_p, c_longlong, c_void_p, c_void_p, c_void_p]),
     "spst_metric_ssim": (c_int, [c_int, c_void_p, c_void_p, c_int, c_int, c_int, c_void_p, c_void_p, c_void_p]),

@@ -9,6 +9,10 @@ namespace spst {
 
 constexpr int kSMs = 148;
 
+// Process-wide count of kernels launched by this library (spst_launch_count); every launch
+// site is written `note_launch(), kernel<<<...>>>(...)`.
+void note_launch();
+
 // Activation storage ("HL16"): fp16 hi plane-set followed by fp16 lo plane-set, each laid out
 // [C_p/8][H][W][8] (8 channels = 16 B per pixel per kgroup).  The stored value is x * 2^e,
 // split so that hi + lo carries ~22 mantissa bits.  Mask storage: uint32 [C_p/32][H][W],

@@ -181,7 +181,7 @@ __global__ void __launch_bounds__(192, 1) first_bwd_tc_kernel(const __grid_const
 cudaError_t launch_first_bwd_tc(const FirstBwdTcArgs& a, cudaStream_t st) {
   cudaFuncSetAttribute(first_bwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
   const int tiles = ((a.W + kOutCols - 1) / kOutCols) * ((a.H + kOutRows - 1) / kOutRows);
-  first_bwd_tc_kernel<<<std::min(tiles, kSMs), 192, kSmem, st>>>(a);
+  note_launch(), first_bwd_tc_kernel<<<std::min(tiles, kSMs), 192, kSmem, st>>>(a);
   return cudaGetLastError();
 }
 

@@ -285,8 +285,8 @@ __global__ void gram64_reduce_kernel(const float* partial, int n_splits, int C, 
 cudaError_t launch_gram64_tc(const GramArgs& a, int n_splits, int C, double inv_scale2, double* S,
                              cudaStream_t stream) {
   cudaFuncSetAttribute(gram64_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Gram64Cfg::SMEM);
-  gram64_tc_kernel<<<n_splits, 192, Gram64Cfg::SMEM, stream>>>(a);
-  gram64_reduce_kernel<<<C, 64, 0, stream>>>(a.partial, n_splits, C, inv_scale2, S);
+  note_launch(), gram64_tc_kernel<<<n_splits, 192, Gram64Cfg::SMEM, stream>>>(a);
+  note_launch(), gram64_reduce_kernel<<<C, 64, 0, stream>>>(a.partial, n_splits, C, inv_scale2, S);
   return cudaGetLastError();
 }
 
@@ -312,14 +312,14 @@ int gram_tc_smem_bytes() { return GramCfg::SMEM; }
 cudaError_t launch_gram_tc(const GramArgs& a, int n_splits, cudaStream_t stream) {
   cudaFuncSetAttribute(gram_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, GramCfg::SMEM);
   dim3 grid(n_splits, a.n_ctile * (a.n_ctile + 1) / 2);
-  gram_tc_kernel<<<grid, 192, GramCfg::SMEM, stream>>>(a);
+  note_launch(), gram_tc_kernel<<<grid, 192, GramCfg::SMEM, stream>>>(a);
   return cudaGetLastError();
 }
 
 cudaError_t launch_gram_reduce(const float* partial, int n_splits, int n_ctile, int C, double inv_scale2,
                                double* S, cudaStream_t stream) {
   dim3 grid((C + 127) / 128, C);
-  gram_reduce_kernel<<<grid, 128, 0, stream>>>(partial, n_splits, n_ctile, C, inv_scale2, S);
+  note_launch(), gram_reduce_kernel<<<grid, 128, 0, stream>>>(partial, n_splits, n_ctile, C, inv_scale2, S);
   return cudaGetLastError();
 }
 

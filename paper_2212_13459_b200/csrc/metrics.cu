@@ -135,9 +135,9 @@ __global__ void __launch_bounds__(256) ssim_partial_kernel(const TA* a, const TB
 cudaError_t launch_metric_sqdiff(bool f64, const void* a, const void* b, long long n, double* partial, double* out,
                                  cudaStream_t st) {
   if (f64)
-    sqdiff_partial_kernel<double><<<red_blocks(), 256, 0, st>>>((const double*)a, (const double*)b, n, partial);
+    note_launch(), sqdiff_partial_kernel<double><<<red_blocks(), 256, 0, st>>>((const double*)a, (const double*)b, n, partial);
   else
-    sqdiff_partial_kernel<float><<<red_blocks(), 256, 0, st>>>((const float*)a, (const float*)b, n, partial);
+    note_launch(), sqdiff_partial_kernel<float><<<red_blocks(), 256, 0, st>>>((const float*)a, (const float*)b, n, partial);
   return launch_sum_partials(partial, 1, out, st);
 }
 
@@ -145,7 +145,7 @@ template <typename TA, typename TB>
 static void launch_ssim_typed(const void* a, const void* b, int h, int w, int c, double* partial, size_t smem,
                               cudaStream_t st) {
   cudaFuncSetAttribute(ssim_partial_kernel<TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  ssim_partial_kernel<TA, TB><<<red_blocks(), 256, smem, st>>>((const TA*)a, (const TB*)b, h, w, c, partial);
+  note_launch(), ssim_partial_kernel<TA, TB><<<red_blocks(), 256, smem, st>>>((const TA*)a, (const TB*)b, h, w, c, partial);
 }
 
 cudaError_t launch_metric_ssim(int f64_mask, const void* a, const void* b, int h, int w, int c, double* partial,

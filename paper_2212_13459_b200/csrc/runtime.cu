@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -268,6 +269,11 @@ struct spst_ctx {
     int _r = (call);       \
     if (_r) return _r;     \
   } while (0)
+
+namespace {
+std::atomic<long long> g_launches{0};
+}  // namespace
+void spst::note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 namespace {
 
@@ -1065,6 +1071,8 @@ void spst_destroy(spst_ctx* ctx) {
 
 const char* spst_last_error(const spst_ctx* ctx) { return ctx ? ctx->msg.c_str() : "null context"; }
 
+long long spst_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
 int spst_timing_enable(spst_ctx* ctx, int on) {
   if (!ctx) return SPST_ERR_CONFIG;
   if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return SPST_ERR_CUDA;
@@ -1396,7 +1404,7 @@ int spst_debug_conv(int device, int mode, int cin, int cout, int H, int W, const
   CK(cudaMemcpy(bd, b32.data(), Np * 4, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(slab_d, slab.data(), slab.size() * 2, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(xd, x_host, (size_t)Kc * H * W * 4, cudaMemcpyHostToDevice));
-  pack_hl_kernel<<<512, 256>>>(xd, Kc, in);
+  note_launch(), pack_hl_kernel<<<512, 256>>>(xd, Kc, in);
   ConvLaunch L;
   L.in = &in;
   L.wslab = slab_d;
@@ -1412,13 +1420,13 @@ int spst_debug_conv(int device, int mode, int cin, int cout, int H, int W, const
   TRY(run_conv(ctx, L));
   CK(cudaDeviceSynchronize());
   if (mode == 1) {
-    unpack_hl_kernel<<<512, 256>>>(pooled, Nc, yd);
+    note_launch(), unpack_hl_kernel<<<512, 256>>>(pooled, Nc, yd);
     CK(cudaMemcpy(y_host, yd, (size_t)Nc * (H / 2) * (W / 2) * 4, cudaMemcpyDeviceToHost));
   } else if (mode == 3) {
-    unpack_mask_kernel<<<512, 256>>>(mask, Nc, H, W, yd);
+    note_launch(), unpack_mask_kernel<<<512, 256>>>(mask, Nc, H, W, yd);
     CK(cudaMemcpy(y_host, yd, (size_t)Nc * H * W * 4, cudaMemcpyDeviceToHost));
   } else {
-    unpack_hl_kernel<<<512, 256>>>(out, Nc, yd);
+    note_launch(), unpack_hl_kernel<<<512, 256>>>(out, Nc, yd);
     CK(cudaMemcpy(y_host, yd, (size_t)Nc * H * W * 4, cudaMemcpyDeviceToHost));
   }
   CK(cudaDeviceSynchronize());
@@ -1441,7 +1449,7 @@ int spst_debug_gram(int device, int C, long long P, const float* f_host, double*
   double* Sd = ctx->dalloc<double>((size_t)C * C);
   if (!t.hi || !fd || !part || !Sd) return SPST_ERR_OOM;
   CK(cudaMemcpy(fd, f_host, (size_t)C * P * 4, cudaMemcpyHostToDevice));
-  pack_hl_kernel<<<512, 256>>>(fd, C, t);
+  note_launch(), pack_hl_kernel<<<512, 256>>>(fd, C, t);
   GramArgs g{};
   if (!map_gram(&g.tm_hi, t.hi, P, P, Cp / 8) || !map_gram(&g.tm_lo, t.lo(), P, P, Cp / 8)) return SPST_ERR_CUDA;
   g.C_p = Cp;

@@ -613,13 +613,13 @@ __global__ void resize_bilinear_kernel(const float* in, int h, int w, int c, int
 cudaError_t launch_image_hl(const ImageHLArgs& a, cudaStream_t st) {
   const long long n = (long long)a.Hl * a.Wp;
   const int blocks = (int)std::min<long long>((n + 255) / 256, 148LL * 8);
-  image_hl_kernel<<<blocks, 256, 0, st>>>(a);
+  note_launch(), image_hl_kernel<<<blocks, 256, 0, st>>>(a);
   return cudaGetLastError();
 }
 
 cudaError_t launch_first_conv_bwd(const FirstConvBwdArgs& a, cudaStream_t st) {
   dim3 grid((a.g.W + FC_BX - 1) / FC_BX, (a.g.H + FC_BY - 1) / FC_BY);
-  first_conv_bwd_kernel<<<grid, 256, 0, st>>>(a);
+  note_launch(), first_conv_bwd_kernel<<<grid, 256, 0, st>>>(a);
   return cudaGetLastError();
 }
 
@@ -627,13 +627,13 @@ cudaError_t launch_fold_grad(const float* gimg, int Hl, int Wp, int row_off, int
                              float* grad, cudaStream_t st) {
   const long long n = (long long)(r1 - r0) * w;
   if (n <= 0) return cudaSuccess;
-  fold_grad_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(gimg, Hl, Wp, row_off, h, w, r0, r1, grad);
+  note_launch(), fold_grad_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(gimg, Hl, Wp, row_off, h, w, r0, r1, grad);
   return cudaGetLastError();
 }
 
 cudaError_t launch_pool2_hl(const HL16& in, const HL16& out, unsigned int* amax, cudaStream_t st) {
   const long long n = (long long)(in.C_p / 8) * out.H * out.W;
-  pool2_hl_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(in, out, amax);
+  note_launch(), pool2_hl_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(in, out, amax);
   return cudaGetLastError();
 }
 
@@ -641,68 +641,68 @@ cudaError_t launch_colsum_reduce(const float* partial, int rows, int C, int stri
                                  cudaStream_t st) {
   const int rows_per = (rows + kColsumChunks - 1) / kColsumChunks;
   const int chunks = (rows + rows_per - 1) / rows_per;
-  colsum_stage1_kernel<<<dim3((C + 31) / 32, chunks), dim3(32, 8), 0, st>>>(partial, rows, C, stride, rows_per, mid);
-  colsum_stage2_kernel<<<(C + 127) / 128, 128, 0, st>>>(mid, chunks, C, sums);
+  note_launch(), colsum_stage1_kernel<<<dim3((C + 31) / 32, chunks), dim3(32, 8), 0, st>>>(partial, rows, C, stride, rows_per, mid);
+  note_launch(), colsum_stage2_kernel<<<(C + 127) / 128, 128, 0, st>>>(mid, chunks, C, sums);
   return cudaGetLastError();
 }
 
 cudaError_t launch_style_vec(const StyleCoefArgs& a, cudaStream_t st) {
-  style_vec_kernel<<<1, 256, 0, st>>>(a);
+  note_launch(), style_vec_kernel<<<1, 256, 0, st>>>(a);
   return cudaGetLastError();
 }
 
 cudaError_t launch_style_mat(const StyleCoefArgs& a, cudaStream_t st) {
-  style_mat_kernel<<<a.C, 256, 0, st>>>(a);
+  note_launch(), style_mat_kernel<<<a.C, 256, 0, st>>>(a);
   return cudaGetLastError();
 }
 
 cudaError_t launch_sum_partials(const double* partial, int nk, double* out, cudaStream_t st) {
-  finish_sums_kernel<<<1, 32, 0, st>>>(partial, kRedBlocks, nk, out);
+  note_launch(), finish_sums_kernel<<<1, 32, 0, st>>>(partial, kRedBlocks, nk, out);
   return cudaGetLastError();
 }
 
 cudaError_t launch_content_sqdiff(const HL16& v, const HL16& u, int C, int r0, int r1, double* partial,
                                   double* out, cudaStream_t st) {
-  content_sqdiff_kernel<<<kRedBlocks, 256, 0, st>>>(v, u, C, r0, r1, partial);
-  finish_sums_kernel<<<1, 32, 0, st>>>(partial, kRedBlocks, 1, out);
+  note_launch(), content_sqdiff_kernel<<<kRedBlocks, 256, 0, st>>>(v, u, C, r0, r1, partial);
+  note_launch(), finish_sums_kernel<<<1, 32, 0, st>>>(partial, kRedBlocks, 1, out);
   return cudaGetLastError();
 }
 
 cudaError_t launch_dots(int f64, const void* a0, const void* b0, const void* a1, const void* b1, const void* a2,
                         const void* b2, long long n, double* partial, double* out, cudaStream_t st) {
   if (f64)
-    dot3_partial_kernel<double><<<kRedBlocks, kRedThreads, 0, st>>>(
+    note_launch(), dot3_partial_kernel<double><<<kRedBlocks, kRedThreads, 0, st>>>(
         (const double*)a0, (const double*)b0, (const double*)a1, (const double*)b1, (const double*)a2,
         (const double*)b2, n, partial);
   else
-    dot3_partial_kernel<float><<<kRedBlocks, kRedThreads, 0, st>>>((const float*)a0, (const float*)b0,
+    note_launch(), dot3_partial_kernel<float><<<kRedBlocks, kRedThreads, 0, st>>>((const float*)a0, (const float*)b0,
                                                                    (const float*)a1, (const float*)b1,
                                                                    (const float*)a2, (const float*)b2, n, partial);
   const int nk = 1 + (a1 != nullptr) + (a2 != nullptr);
-  finish_sums_kernel<<<1, 32, 0, st>>>(partial, kRedBlocks, nk, out);
+  note_launch(), finish_sums_kernel<<<1, 32, 0, st>>>(partial, kRedBlocks, nk, out);
   return cudaGetLastError();
 }
 
 cudaError_t launch_absmax(int f64, const void* a, long long n, double* partial, double* out, cudaStream_t st) {
   if (f64)
-    absmax_partial_kernel<double><<<kRedBlocks, kRedThreads, 0, st>>>((const double*)a, n, partial);
+    note_launch(), absmax_partial_kernel<double><<<kRedBlocks, kRedThreads, 0, st>>>((const double*)a, n, partial);
   else
-    absmax_partial_kernel<float><<<kRedBlocks, kRedThreads, 0, st>>>((const float*)a, n, partial);
-  finish_max_kernel<<<1, 1, 0, st>>>(partial, kRedBlocks, out);
+    note_launch(), absmax_partial_kernel<float><<<kRedBlocks, kRedThreads, 0, st>>>((const float*)a, n, partial);
+  note_launch(), finish_max_kernel<<<1, 1, 0, st>>>(partial, kRedBlocks, out);
   return cudaGetLastError();
 }
 
 cudaError_t launch_axpy_dot(int f64, const AxpyDotArgs& a, cudaStream_t st) {
   if (f64)
-    axpy_dot_kernel<double><<<kRedBlocks, kRedThreads, 0, st>>>(a);
+    note_launch(), axpy_dot_kernel<double><<<kRedBlocks, kRedThreads, 0, st>>>(a);
   else
-    axpy_dot_kernel<float><<<kRedBlocks, kRedThreads, 0, st>>>(a);
+    note_launch(), axpy_dot_kernel<float><<<kRedBlocks, kRedThreads, 0, st>>>(a);
   return cudaGetLastError();
 }
 
 cudaError_t launch_twoloop_scalar(const double* dot, double rho, int mode, double* alpha_i, double* coef,
                                   cudaStream_t st) {
-  twoloop_scalar_kernel<<<1, 1, 0, st>>>(dot, rho, mode, alpha_i, coef);
+  note_launch(), twoloop_scalar_kernel<<<1, 1, 0, st>>>(dot, rho, mode, alpha_i, coef);
   return cudaGetLastError();
 }
 
@@ -710,32 +710,32 @@ cudaError_t launch_twoloop_scalar(const double* dot, double rho, int mode, doubl
 
 cudaError_t launch_axpy(int f64, const void* x, const void* d, double t, long long n, void* out, cudaStream_t st) {
   if (f64)
-    axpy_kernel<double><<<4 * kSMs, 512, 0, st>>>((const double*)x, (const double*)d, t, n, (double*)out);
+    note_launch(), axpy_kernel<double><<<4 * kSMs, 512, 0, st>>>((const double*)x, (const double*)d, t, n, (double*)out);
   else
-    axpy_kernel<float><<<4 * kSMs, 512, 0, st>>>((const float*)x, (const float*)d, (float)t, n, (float*)out);
+    note_launch(), axpy_kernel<float><<<4 * kSMs, 512, 0, st>>>((const float*)x, (const float*)d, (float)t, n, (float*)out);
   return cudaGetLastError();
 }
 
 cudaError_t launch_sy(int f64, const void* xt, const void* x, const void* gt, const void* g, long long n, void* s,
                       void* y, double* partial, double* out, cudaStream_t st) {
   if (f64)
-    sy_kernel<double><<<kRedBlocks, kRedThreads, 0, st>>>((const double*)xt, (const double*)x, (const double*)gt,
+    note_launch(), sy_kernel<double><<<kRedBlocks, kRedThreads, 0, st>>>((const double*)xt, (const double*)x, (const double*)gt,
                                                           (const double*)g, n, (double*)s, (double*)y, partial);
   else
-    sy_kernel<float><<<kRedBlocks, kRedThreads, 0, st>>>((const float*)xt, (const float*)x, (const float*)gt,
+    note_launch(), sy_kernel<float><<<kRedBlocks, kRedThreads, 0, st>>>((const float*)xt, (const float*)x, (const float*)gt,
                                                          (const float*)g, n, (float*)s, (float*)y, partial);
-  finish_sums_kernel<<<1, 32, 0, st>>>(partial, kRedBlocks, 3, out);
+  note_launch(), finish_sums_kernel<<<1, 32, 0, st>>>(partial, kRedBlocks, 3, out);
   return cudaGetLastError();
 }
 
 cudaError_t launch_resize_down(const float* in, int h, int w, int c, int f, float* out, cudaStream_t st) {
-  resize_down_kernel<<<4 * kSMs, 256, 0, st>>>(in, h, w, c, f, out);
+  note_launch(), resize_down_kernel<<<4 * kSMs, 256, 0, st>>>(in, h, w, c, f, out);
   return cudaGetLastError();
 }
 
 cudaError_t launch_resize_bilinear(const float* in, int h, int w, int c, int oh, int ow, float* out,
                                    cudaStream_t st) {
-  resize_bilinear_kernel<<<4 * kSMs, 256, 0, st>>>(in, h, w, c, oh, ow, out);
+  note_launch(), resize_bilinear_kernel<<<4 * kSMs, 256, 0, st>>>(in, h, w, c, oh, ow, out);
   return cudaGetLastError();
 }
 

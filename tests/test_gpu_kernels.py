@@ -9,6 +9,7 @@ pytestmark = pytest.mark.gpu
 
 import spst_oracle as O  # noqa: E402
 from paper_2212_13459_b200 import _native  # noqa: E402
+import paper_2212_13459_b200 as spst  # noqa: E402
 from conftest import golden, rel_l2  # noqa: E402
 
 # every conv shape of VGG-19 (reduced spatial size) + TinyNet-like odd channel counts
@@ -111,3 +112,30 @@ def test_vector_kernels_f32_f64():
         np.testing.assert_array_equal(sn, (a - b).cpu().numpy())
         assert ys == pytest.approx(float(yn @ sn), rel=1e-12)
         assert ss == pytest.approx(float(sn @ sn), rel=1e-12)
+
+
+# ---------------------------------------------------------------- measurement hooks
+@pytest.mark.gpu
+def test_launch_counter_and_timer(tiny_spec):
+    """spst_launch_count counts our kernels; the engine's launch timer brackets the tensor-core
+    launches of an evaluation with events and reports algorithmic FLOPs (bench.py's roofline)."""
+    from paper_2212_13459_b200 import _native as nat
+    rng = np.random.default_rng(0)
+    u, v, x = (rng.random((64, 96, 3)).astype(np.float32) for _ in range(3))
+    p = spst.build_problem(u, v, tiny_spec, spst.default_loss_weights(tiny_spec))
+    spst.loss_grad(x, p)  # warm (range exponents known)
+    eng = p.engine
+    n0 = int(nat.lib().spst_launch_count())
+    eng.timing_enable(True)
+    spst.loss_grad(x, p)
+    t = eng.timing_read()
+    eng.timing_enable(False)
+    n1 = int(nat.lib().spst_launch_count())
+    assert n1 - n0 >= 10
+    assert set(t) <= {"conv3x3_tc<128>", "conv3x3_tc<64>", "gram_tc"} and "conv3x3_tc<64>" in t
+    for ms, flops, n in t.values():
+        assert ms > 0 and n > 0 and flops >= 0
+    # disabled timer records nothing
+    eng.timing_enable(False)
+    spst.loss_grad(x, p)
+    assert eng.timing_read() == {}

@@ -228,11 +228,32 @@ struct spst_ctx {
     return fail(e == cudaErrorMemoryAllocation ? SPST_ERR_OOM : SPST_ERR_CUDA,
                 std::string(where) + ": " + cudaGetErrorString(e));
   }
+  // Bound (per image size) buffers come from a per-context stream-ordered pool that keeps freed
+  // memory reserved: a multiscale run re-binds at every scale and would otherwise return and
+  // re-map tens of GB through the driver each time.  Persistent buffers (weights) use cudaMalloc.
+  cudaMemPool_t pool = nullptr;
+  bool pool_ready() {
+    if (pool) return true;
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = device;
+    if (cudaMemPoolCreate(&pool, &props) != cudaSuccess) {
+      cudaGetLastError();
+      pool = nullptr;
+      return false;
+    }
+    uint64_t keep_all = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep_all);
+    return true;
+  }
   template <typename T>
   T* dalloc(size_t n, bool keep = false) {
     void* p = nullptr;
     if (n == 0) n = 1;
-    if (cudaMalloc(&p, n * sizeof(T)) != cudaSuccess) {
+    const cudaError_t e = (!keep && pool_ready()) ? cudaMallocFromPoolAsync(&p, n * sizeof(T), pool, stream)
+                                                  : cudaMalloc(&p, n * sizeof(T));
+    if (e != cudaSuccess) {
       cudaGetLastError();
       return nullptr;
     }
@@ -243,7 +264,8 @@ struct spst_ctx {
   void release_bound() {
     if (stream) cudaStreamSynchronize(stream);
     cudaDeviceSynchronize();
-    for (void* p : allocs) cudaFree(p);
+    for (void* p : allocs) pool ? cudaFreeAsync(p, stream) : cudaFree(p);
+    if (pool) cudaStreamSynchronize(stream);
     allocs.clear();
     alloc_bytes = 0;
     bound = false;
@@ -928,16 +950,16 @@ int bind_alloc(spst_ctx* ctx) {
       if (!t.S || !t.s || !t.mu || !t.sd || !t.ratio || !t.row_loss || !t.row_mmax || !t.ms_loss || !t.degenerate ||
           !t.bvec || !t.xw || !t.gram_partial || !t.colsum_partial || !t.colsum_mid)
         return ctx->fail(SPST_ERR_OOM, "statistics buffers");
-      CK(cudaMemset(t.bvec, 0, Cp * 4));
-      CK(cudaMemset(t.s, 0, Cp * 8));
+      CK(cudaMemsetAsync(t.bvec, 0, Cp * 4, ctx->stream));
+      CK(cudaMemsetAsync(t.s, 0, Cp * 8, ctx->stream));
       if (!t.Gr) {  // reference buffers persist across binds
         t.Gr = ctx->dalloc<double>((size_t)C * C, true);
         t.mur = ctx->dalloc<double>(C, true);
         t.sdr = ctx->dalloc<double>(C, true);
         if (!t.Gr || !t.mur || !t.sdr) return ctx->fail(SPST_ERR_OOM, "reference statistics");
-        CK(cudaMemset(t.Gr, 0, (size_t)C * C * 8));
-        CK(cudaMemset(t.mur, 0, C * 8));
-        CK(cudaMemset(t.sdr, 0, C * 8));
+        CK(cudaMemsetAsync(t.Gr, 0, (size_t)C * C * 8, ctx->stream));
+        CK(cudaMemsetAsync(t.mur, 0, C * 8, ctx->stream));
+        CK(cudaMemsetAsync(t.sdr, 0, C * 8, ctx->stream));
       }
     }
   }
@@ -959,14 +981,15 @@ int bind_alloc(spst_ctx* ctx) {
   ctx->zero_xw = ctx->dalloc<__half>((size_t)max_cp * max_cp * 2);
   if (!ctx->addend.hi || !ctx->gimg || !ctx->amax_d || !ctx->content_partial || !ctx->zero_xw)
     return ctx->fail(SPST_ERR_OOM, "workspace");
-  CK(cudaMemset(ctx->zero_xw, 0, (size_t)max_cp * max_cp * 2 * sizeof(__half)));
-  CK(cudaMemset(ctx->amax_d, 0, 16 * n + 16));
+  CK(cudaMemsetAsync(ctx->zero_xw, 0, (size_t)max_cp * max_cp * 2 * sizeof(__half), ctx->stream));
+  CK(cudaMemsetAsync(ctx->amax_d, 0, 16 * n + 16, ctx->stream));
   if (ctx->content_stage >= 0) {
     const Stage& s = ctx->stages[ctx->content_stage];
     ctx->content_u = hl_shape(s.cout_p, s.H, s.W);
     ctx->content_u.hi = ctx->dalloc<__half>((size_t)s.cout_p * s.H * s.W * 2);
     if (!ctx->content_u.hi) return ctx->fail(SPST_ERR_OOM, "content target");
   }
+  CK(cudaStreamSynchronize(ctx->stream));  // pool allocations and clears are stream-ordered
   return SPST_OK;
 }
 
@@ -1065,6 +1088,7 @@ void spst_destroy(spst_ctx* ctx) {
     cudaEventDestroy(t.b);
   }
   ctx->release_bound();
+  if (ctx->pool) cudaMemPoolDestroy(ctx->pool);
   for (void* p : ctx->persistent) cudaFree(p);
   delete ctx;
 }

@@ -32,7 +32,10 @@
 
 namespace spst {
 
-template <int N>
+// RES ("resident weights", 64-channel GEMMs whose conv slab fits): the whole weight slab is
+// loaded once per CTA behind two activation-only stages, instead of re-streaming 37 KB per
+// chunk per tile -- those layers were bound by their operand loads.
+template <int N, bool RES = false>
 struct ConvCfg {
   static constexpr int MT = 2;                      // output rows per tile (M = MT x 128 px)
   static constexpr int PITCH = 136;                 // 128 output px + 2 halo px, padded to 17 x 128 B
@@ -50,14 +53,20 @@ struct ConvCfg {
   static constexpr int XA_PLANE = MT * 128 * 16;    // extra-K operand: MT rows x 128 px, 8 ch
   static constexpr int XA_HALF = XKG * XA_PLANE;
   static constexpr int XB_BYTES = 2 * XKG * N * 16; // extra-K slab: hi/lo x XKG kgroups
-  static constexpr int STAGE = ((A_BYTES + B_BYTES + 1023) / 1024) * 1024;
-  static constexpr int STAGES = N == 128 ? 2 : 3;
+  // (a resident-mode stage holds an activation window or an extra-K operand + its slab)
+  static constexpr int STAGE_BYTES = RES ? (A_BYTES > 2 * XA_HALF + XB_BYTES ? A_BYTES : 2 * XA_HALF + XB_BYTES)
+                                         : A_BYTES + B_BYTES;
+  static constexpr int STAGE = ((STAGE_BYTES + 1023) / 1024) * 1024;
+  static constexpr int STAGES = (N == 128 || RES) ? 2 : 3;
+  static constexpr int RES_OFF = STAGES * STAGE;     // resident slab (RES only)
+  static constexpr int RES_MAX = RES ? 147456 : 0;   // up to 4 chunks of N=64 (C_in <= 64)
   static constexpr int NBUF = 512 / (MT * N);       // TMEM chunk buffers (MT rows x N each)
   static constexpr int TMEM_COLS = 512;
-  static constexpr int SMEM = STAGES * STAGE + 1024;
+  static constexpr int SMEM = STAGES * STAGE + RES_MAX + 1024;
   static constexpr int CPG = MT == 2 ? N / 2 : N;   // channels per epilogue warpgroup
-  static constexpr int XB_OFF = 2 * XA_HALF > A_BYTES ? 2 * XA_HALF : A_BYTES;  // extra-K slab offset
+  static constexpr int XB_OFF = (RES || 2 * XA_HALF > A_BYTES) ? 2 * XA_HALF : A_BYTES;  // extra-K slab offset
   static_assert(XB_OFF + XB_BYTES <= STAGE, "extra-K operand and slab must fit one stage");
+  static_assert(SMEM + 2048 <= 232448, "dynamic + static shared memory must fit 227 KB");
   static_assert(2 * STRIP * 16 == PITCH * 16 && (PITCH * 16) % 128 == 0 && A_PLANE % 128 == 0, "strip layout");
 };
 
@@ -334,13 +343,13 @@ __device__ __forceinline__ TileId decode_tile(const ConvArgs& a, int t) {
   return id;
 }
 
-template <int N>
+template <int N, bool RES>
 __global__ void __launch_bounds__(320, 1) conv3x3_tc_kernel(const __grid_constant__ ConvArgs a) {
-  using C = ConvCfg<N>;
+  using C = ConvCfg<N, RES>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ uint64_t full_bar[C::STAGES], empty_bar[C::STAGES];
-  __shared__ uint64_t cfull_bar[C::NBUF], cempty_bar[C::NBUF];
+  __shared__ uint64_t cfull_bar[C::NBUF], cempty_bar[C::NBUF], res_bar;
   __shared__ uint32_t tmem_slot;
 
   const uint32_t warp = warp_id();
@@ -363,6 +372,7 @@ __global__ void __launch_bounds__(320, 1) conv3x3_tc_kernel(const __grid_constan
       mbar_init(&cfull_bar[b], 1);
       mbar_init(&cempty_bar[b], 8);
     }
+    mbar_init(&res_bar, 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<C::TMEM_COLS>(&tmem_slot);
@@ -381,6 +391,12 @@ __global__ void __launch_bounds__(320, 1) conv3x3_tc_kernel(const __grid_constan
     const int s_hl = lane / (4 * C::RIN), s_p = (lane / (2 * C::RIN)) & 1, s_r = (lane >> 1) % C::RIN, s_h = lane & 1;
     const uint32_t s_off = s_hl * C::A_HALF + s_p * C::A_PLANE + (s_r * C::PITCH + s_h * 64) * 16;
     const void* s_map = s_hl ? (const void*)&a.tm_r_lo : (const void*)&a.tm_r_hi;
+    if constexpr (RES) {  // the whole conv slab (one N-tile), once per CTA
+      if (lane == 0) {
+        mbar_arrive_expect_tx(&res_bar, (uint32_t)a.n_kc * C::B_BYTES);
+        bulk_load(smem + C::RES_OFF, a.wgt, (uint32_t)a.n_kc * C::B_BYTES, &res_bar);
+      }
+    }
     uint32_t g = 0;
     for (int t = first; t < n_tiles; t += step) {
       const TileId id = decode_tile(a, t);
@@ -394,7 +410,7 @@ __global__ void __launch_bounds__(320, 1) conv3x3_tc_kernel(const __grid_constan
         int ci;
         const bool extra = chunk_is_extra(c, a.n_kc, ci);
         if (!extra) {
-          if (lane == 0) mbar_arrive_expect_tx(&full_bar[s], C::A_BYTES + C::B_BYTES);
+          if (lane == 0) mbar_arrive_expect_tx(&full_bar[s], C::A_BYTES + (RES ? 0 : C::B_BYTES));
           __syncwarp();
           if (lane < 8 * C::RIN)
             tma_load_3d(st + s_off, s_map, &full_bar[s], 2 * (x0 - 1) + 128 * s_h, y0 - 1 + s_r, 2 * ci + s_p);
@@ -403,7 +419,7 @@ __global__ void __launch_bounds__(320, 1) conv3x3_tc_kernel(const __grid_constan
           tma_load_4d(st, &a.tm_v_hi, &full_bar[s], 0, x0, y0, C::XKG * ci);
           tma_load_4d(st + C::XA_HALF, &a.tm_v_lo, &full_bar[s], 0, x0, y0, C::XKG * ci);
         }
-        if (lane == 0) {
+        if (lane == 0 && (extra || !RES)) {
           const uint8_t* bsrc = extra ? a.xwgt + ((size_t)nt * a.n_xkc + ci) * C::XB_BYTES
                                       : a.wgt + ((size_t)nt * a.n_kc + ci) * C::B_BYTES;
           const uint32_t bbytes = extra ? C::XB_BYTES : C::B_BYTES;
@@ -417,6 +433,7 @@ __global__ void __launch_bounds__(320, 1) conv3x3_tc_kernel(const __grid_constan
     // one elected lane issues; see umma_f16_ws)
     {
       const uint32_t idesc = make_idesc_f16(128, N, 0, 0, 0);
+      if constexpr (RES) mbar_wait(&res_bar, 0);
       uint32_t g = 0, gq = 0;  // chunk counter (smem stages), group counter (TMEM buffers)
       for (int t = first; t < n_tiles; t += step) {
         for (int c = 0; c < n_chunks; ++c, ++g) {
@@ -429,9 +446,9 @@ __global__ void __launch_bounds__(320, 1) conv3x3_tc_kernel(const __grid_constan
           __syncwarp();
           tc_fence_after();
           const uint32_t st = smem_u32(smem + s * C::STAGE);
-          const uint32_t bb = st + C::A_BYTES;
           int ci;
           const bool extra = chunk_is_extra(c, a.n_kc, ci);
+          const uint32_t bb = RES ? smem_u32(smem + C::RES_OFF) + (uint32_t)ci * C::B_BYTES : st + C::A_BYTES;
           const uint32_t dcol = tmem_base + b * C::MT * N;
           // descriptor arithmetic: start-address field = addr >> 4 in the low bits, so an
           // offset of k bytes is an add of k >> 4 on the precomputed 64-bit descriptor
@@ -575,16 +592,23 @@ int conv_tc_smem_bytes(int N) { return N == 128 ? ConvCfg<128>::SMEM : ConvCfg<6
 int conv_tc_rows(int N) { return N == 128 ? ConvCfg<128>::MT : ConvCfg<64>::MT; }
 int conv_tc_xkg(int N) { return N == 128 ? ConvCfg<128>::XKG : ConvCfg<64>::XKG; }
 
-template <int N>
+template <int N, bool RES>
 static cudaError_t launch_one(const ConvArgs& a, int grid, cudaStream_t stream) {
-  auto k = conv3x3_tc_kernel<N>;
-  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, ConvCfg<N>::SMEM);
-  note_launch(), k<<<grid, 320, ConvCfg<N>::SMEM, stream>>>(a);
+  auto k = conv3x3_tc_kernel<N, RES>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, ConvCfg<N, RES>::SMEM);
+  note_launch(), k<<<grid, 320, ConvCfg<N, RES>::SMEM, stream>>>(a);
   return cudaGetLastError();
 }
 
+// resident: 64-channel GEMM whose whole conv slab (one N-tile, n_kc chunks) fits in smem
+bool conv_tc_resident_ok(int N, int n_ntiles, int n_kc) {
+  return N == 64 && n_ntiles == 1 && n_kc >= 1 && n_kc * ConvCfg<64, true>::B_BYTES <= ConvCfg<64, true>::RES_MAX;
+}
+
 cudaError_t launch_conv_tc(const ConvArgs& a, int N, int grid, cudaStream_t stream) {
-  return N == 128 ? launch_one<128>(a, grid, stream) : launch_one<64>(a, grid, stream);
+  if (N == 128) return launch_one<128, false>(a, grid, stream);
+  return conv_tc_resident_ok(N, a.n_ntiles, a.n_kc) ? launch_one<64, true>(a, grid, stream)
+                                                    : launch_one<64, false>(a, grid, stream);
 }
 
 }  // namespace spst

@@ -36,8 +36,8 @@ from .tiling import margin_for_exact_gradient, stripes
 def init(local_rank: int | None = None, backend: str | None = None):
     """Initialise the default process group from torchrun's env (MASTER_ADDR=127.0.0.1)."""
     if not dist.is_initialized():
-        if backend is None:
-            backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if backend is None:  # SPST_DIST_BACKEND: functional multi-rank checks on one device (gloo)
+            backend = os.environ.get("SPST_DIST_BACKEND") or ("nccl" if torch.cuda.is_available() else "gloo")
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         if backend == "nccl" and local_rank is not None:
             torch.cuda.set_device(local_rank)

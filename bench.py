@@ -233,13 +233,12 @@ def run_ours(args):
         value = iters / (ms / 1e3)
         achieved = flops_eval / (eval_ms / 1e3) / 1e12 / world if eval_ms else None
         line = {
-            "metric": f"L-BFGS iters/sec at {H}x{W} (tiled VGG-19)",
+            "metric": metric_name(H, W),
             "value": value, "unit": "iters/s", "n_gpus": world, "steps": iters, "warmup": args.warmup,
             "ms_per_step": ms / iters, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "fp16x3 (fp16 hi/lo split operands, fp32 accumulation) / f32 vectors",
             "data": "synthetic (seeded content/style, calibrated seeded VGG-19 weights)",
-            "config": {"workload": f"{args.config}: single-scale L-BFGS at {H}x{W} content, {sh}x{sw} style, "
-                                   "VGG-19 to relu5_1, m=10, default loss weights",
+            "config": {"workload": workload_name(args.config, H, W, sh, sw),
                        "image": [H, W], "style": [sh, sw], "history": 10, "parallelism": f"row-stripes x{world}",
                        "l2_flush": "not needed (working set ~80 GB >> 126 MB L2)",
                        "evals_per_iter": evals_per_iter, "setup_s": setup_s},
@@ -347,6 +346,15 @@ def cpu_baseline(args, H, W, sh, sw, evals_per_iter, sample_only=False):
                       f"x{area / (side * side):.1f} and {evals_per_iter:.2f} evals/iter"}
 
 
+def metric_name(H, W):
+    return f"L-BFGS iters/sec at {H}x{W} (tiled VGG-19)"
+
+
+def workload_name(config, H, W, sh, sw):
+    return (f"{config}: single-scale L-BFGS at {H}x{W} content, {sh}x{sw} style, VGG-19 to relu5_1, m=10, "
+            "default loss weights")
+
+
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
@@ -363,11 +371,12 @@ def run_reference(args):
             vals.append(r["value"])
         last = r
     value = statistics.mean(vals) if vals else last["value"]
-    line = {"metric": "L-BFGS iters/sec at 6048x8064 (tiled VGG-19)", "value": value, "unit": "iters/s",
+    line = {"metric": metric_name(H, W), "value": value, "unit": "iters/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / value,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic", "impl": "reference",
-            "config": {"workload": f"{args.config}: single-scale L-BFGS at {H}x{W}, {sh}x{sw} style, VGG-19, m=10"},
+            "config": {"workload": workload_name(args.config, H, W, sh, sw), "image": [H, W], "style": [sh, sw],
+                       "history": 10},
             "cpu_baseline": dict(last, value=value),
             "e2e": {"value": value, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))

@@ -6,7 +6,8 @@ with gamma = <s,y>/<y,y> of the newest pair, Armijo backtracking (c1 = 1e-4, shr
 oldest-pair eviction, zero step + drop-oldest on line-search failure, NonFiniteError with
 the last finite iterate.  The vectors (x, g, d, s/y history) stay in HBM; every pass is a
 libspst kernel with f64 fixed-order reductions; the alpha/beta coefficients of the two-loop
-live in device memory, so a direction costs 2m+1 fused kernels and no host sync.  The
+live in device memory, so a direction costs 2m+1 fused kernels (one native call on a single
+device; each kernel also finishes its dot product and scalar update) and no host sync.  The
 paper's CPU offload of the history (SPEC "state_residency") is unnecessary with 180 GB HBM;
 the knob is accepted and ignored.
 
@@ -155,7 +156,9 @@ class LBFGSState:
 
 
 def _two_loop(g, state: LBFGSState, vec: _Vec, out, allreduce=None):
-    """-H g into `out` (lbfgs.py:68-83) as 2m+1 fused axpy+dot kernels with device scalars."""
+    """-H g into `out` (lbfgs.py:68-83) as 2m+1 fused axpy+dot kernels with device scalars:
+    one native call (spst_vec_two_loop) on a single device, step by step with an all-reduce
+    per dot product across ranks."""
     m = len(state.s_hist)
     if m == 0:
         return out.copy_(g).neg_()

@@ -148,6 +148,21 @@ struct AxpyDotArgs {
   int mode = 0;
 };
 
+// Whole two-loop in one cooperative launch (spst_vec_two_loop on one device)
+constexpr int kTwoLoopMaxHist = 128;
+struct TwoLoopArgs {
+  const void* g;
+  void* out;
+  const void* s[kTwoLoopMaxHist];  // oldest first
+  const void* y[kTwoLoopMaxHist];
+  double rho[kTwoLoopMaxHist];
+  double gamma;
+  int m;
+  long long n;
+  double* partial;  // 2 x red_blocks() doubles
+};
+cudaError_t launch_two_loop_coop(int f64, const TwoLoopArgs& a, cudaStream_t st);
+
 // ---------------------------------------------------------------- launchers
 cudaError_t launch_conv_tc(const ConvArgs& a, int N, int grid, cudaStream_t stream);
 int conv_tc_smem_bytes(int N);

@@ -1312,6 +1312,27 @@ int spst_vec_two_loop(int f64, const void* g, void* out, const void* const* s_ve
   // so the results equal the 3-kernel-per-step form bit for bit.  Pairs oldest first.
   if (m < 1 || n < 0 || !g || !out || !ticket) return SPST_ERR_SHAPE;
   cudaStream_t st = (cudaStream_t)stream;
+  static const bool per_step = [] {
+    const char* e = getenv("SPST_TWOLOOP_STEPS");
+    return e && atoi(e) != 0;
+  }();
+  if (!per_step && m <= kTwoLoopMaxHist) {  // one cooperative launch (same bits as the steps below)
+    TwoLoopArgs ta{};
+    ta.g = g;
+    ta.out = out;
+    for (int i = 0; i < m; ++i) {
+      ta.s[i] = s_vecs[i];
+      ta.y[i] = y_vecs[i];
+      ta.rho[i] = rho[i];
+    }
+    ta.gamma = gamma;
+    ta.m = m;
+    ta.n = n;
+    ta.partial = partial;
+    const cudaError_t e = launch_two_loop_coop(f64, ta, st);
+    if (e == cudaSuccess) return SPST_OK;
+    if (e != cudaErrorNotSupported) return SPST_ERR_CUDA;
+  }
   auto step = [&](const void* qi, const void* v, double cscale, const void* w, int i, int mode) -> bool {
     AxpyDotArgs a{qi, out, v, coef, cscale, w, n, partial};
     if (w) {

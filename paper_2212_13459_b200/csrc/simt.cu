@@ -10,10 +10,13 @@
 //   * area downsampling and half-pixel bilinear resampling (tensorops.py:136-185)
 #include <algorithm>
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "sm100.cuh"
 
 namespace spst {
+namespace cg = cooperative_groups;
 
 // ------------------------------------------------------------------------------------------
 // first conv (C_in = 3)
@@ -382,12 +385,24 @@ __global__ void __launch_bounds__(kRedThreads) dot3_partial_kernel(const T* a0, 
 }
 
 // out[k] = sum_b partial[k*nb + b], k < nk (fixed order)
-__global__ void finish_sums_kernel(const double* partial, int nb, int nk, double* out) {
-  const int k = threadIdx.x;
-  if (k >= nk) return;
+// The library's one fixed reduction order for block partials (whole warp; every lane returns
+// the total): lane l sums p[l], p[l+32], ... in order, then a fixed xor butterfly.  Used by the
+// finish kernel, the fused two-loop finish and the cooperative two-loop, so all agree bitwise.
+__device__ __forceinline__ double warp_fixed_sum(const double* p, int nb) {
+  const int l = threadIdx.x & 31;
   double acc = 0.0;
-  for (int b = 0; b < nb; ++b) acc += partial[(size_t)k * nb + b];
-  out[k] = acc;
+  for (int b = l; b < nb; b += 32) acc += __ldcg(p + b);  // L2: other blocks wrote these this launch
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  return acc;
+}
+
+// out[k] = fixed-order sum of partial[k*nb .. k*nb+nb), one warp per quantity
+__global__ void finish_sums_kernel(const double* partial, int nb, int nk, double* out) {
+  const int k = threadIdx.x >> 5;
+  if (k >= nk) return;
+  const double t = warp_fixed_sum(partial + (size_t)k * nb, nb);
+  if ((threadIdx.x & 31) == 0) out[k] = t;
 }
 
 template <typename T>
@@ -413,21 +428,17 @@ __global__ void finish_max_kernel(const double* partial, int nb, double* out) {
   *out = m;
 }
 
-// Two-loop step: q_out = cscale * (q_in + coef[0] * v); partial <w, q_out>.
+// Two-loop step body (one block's slice): q_out = cscale * (q_in + c * v); returns the block's
+// partial <w, q_out> in thread 0 (0 elsewhere).  Shared by the per-step and cooperative kernels so
+// both produce identical bits.
 template <typename T>
-__global__ void __launch_bounds__(kRedThreads) axpy_dot_kernel(AxpyDotArgs a) {
-  __shared__ double sh[32];
-  const T* qi = reinterpret_cast<const T*>(a.q_in);
-  T* qo = reinterpret_cast<T*>(a.q_out);
-  const T* v = reinterpret_cast<const T*>(a.v);
-  const T* w = reinterpret_cast<const T*>(a.w);
-  const T c = v ? (T)(*a.coef) : (T)0;
-  const T cs = (T)a.cscale;
+__device__ __forceinline__ double axpy_dot_body(const T* qi, T* qo, const T* v, T c, T cs, const T* w, long long n,
+                                                double* sh) {
   double s = 0.0;
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x, nth = (long long)gridDim.x * blockDim.x;
   long long start = 0;
   if constexpr (sizeof(T) == 4) {  // float4 body
-    const long long n4 = a.n / 4;
+    const long long n4 = n / 4;
     for (long long i = tid; i < n4; i += nth) {
       float4 q = reinterpret_cast<const float4*>(qi)[i];
       if (v) {
@@ -449,37 +460,95 @@ __global__ void __launch_bounds__(kRedThreads) axpy_dot_kernel(AxpyDotArgs a) {
     }
     start = n4 * 4;
   }
-  for (long long i = start + tid; i < a.n; i += nth) {
+  for (long long i = start + tid; i < n; i += nth) {
     T q = qi[i];
     if (v) q = q + c * v[i];
     q = q * cs;
     qo[i] = q;
     if (w) s += (double)w[i] * (double)q;
   }
+  return w ? block_sum(s, sh) : 0.0;
+}
+
+// Two-loop step: q_out = cscale * (q_in + coef[0] * v); partial <w, q_out>.
+template <typename T>
+__global__ void __launch_bounds__(kRedThreads) axpy_dot_kernel(AxpyDotArgs a) {
+  __shared__ double sh[32];
+  const T* qi = reinterpret_cast<const T*>(a.q_in);
+  T* qo = reinterpret_cast<T*>(a.q_out);
+  const T* v = reinterpret_cast<const T*>(a.v);
+  const T* w = reinterpret_cast<const T*>(a.w);
+  const T c = v ? (T)(*a.coef) : (T)0;
+  const double t = axpy_dot_body<T>(qi, qo, v, c, (T)a.cscale, w, a.n, sh);
   if (w) {
-    const double t = block_sum(s, sh);
     if (threadIdx.x == 0) a.partial[blockIdx.x] = t;
     if (a.alpha_i) {  // fused finish: the last block reduces in block order, then the scalar step
       __shared__ bool last;
       __threadfence();
       if (threadIdx.x == 0) last = atomicAdd(a.ticket, 1u) == gridDim.x - 1;
       __syncthreads();
-      if (last && threadIdx.x == 0) {
+      if (last && threadIdx.x < 32) {
         __threadfence();
-        const volatile double* pv = a.partial;
-        double dot = 0.0;
-        for (unsigned b = 0; b < gridDim.x; ++b) dot += pv[b];
-        double* coef = const_cast<double*>(a.coef);  // read by every block at entry, written here last
-        if (a.mode == 0) {
-          *a.alpha_i = a.rho * dot;
-          *coef = -(*a.alpha_i);
-        } else {
-          *coef = *a.alpha_i - a.rho * dot;
+        const double dot = warp_fixed_sum(a.partial, gridDim.x);
+        if (threadIdx.x == 0) {
+          double* coef = const_cast<double*>(a.coef);  // read by every block at entry, written here last
+          if (a.mode == 0) {
+            *a.alpha_i = a.rho * dot;
+            *coef = -(*a.alpha_i);
+          } else {
+            *coef = *a.alpha_i - a.rho * dot;
+          }
+          *a.ticket = 0u;
         }
-        *a.ticket = 0u;
       }
     }
   }
+}
+
+// The whole two-loop (lbfgs.py:68-83) in one cooperative launch: each step is the body above,
+// then one grid barrier; every block sums the partials in block order and applies the scalar
+// update itself (alpha kept in shared memory), so the result equals the per-step kernels bit for
+// bit.  Partials are double-buffered, so one barrier per step suffices.
+template <typename T>
+__global__ void __launch_bounds__(kRedThreads, 2) two_loop_coop_kernel(const __grid_constant__ TwoLoopArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double sh[32];
+  __shared__ double alpha[kTwoLoopMaxHist];
+  __shared__ double sdot;
+  T* out = reinterpret_cast<T*>(a.out);
+  double coef = 0.0;
+  int par = 0;
+  auto step = [&](const T* qi, const T* v, double cscale, const T* w, int i, int mode) {
+    const T c = v ? (T)coef : (T)0;
+    const double t = axpy_dot_body<T>(qi, out, v, c, (T)cscale, w, a.n, sh);
+    if (!w) return;
+    double* P = a.partial + par * gridDim.x;
+    if (threadIdx.x == 0) P[blockIdx.x] = t;
+    grid.sync();
+    if (threadIdx.x < 32) {
+      const double dot = warp_fixed_sum(P, gridDim.x);
+      if (threadIdx.x != 0) {
+      } else if (mode == 0) {
+        alpha[i] = a.rho[i] * dot;
+        sdot = -alpha[i];
+      } else {
+        sdot = alpha[i] - a.rho[i] * dot;
+      }
+    }
+    __syncthreads();
+    coef = sdot;
+    __syncthreads();  // sdot is rewritten by the next step
+    par ^= 1;
+  };
+  const int m = a.m;
+  const T* g = reinterpret_cast<const T*>(a.g);
+  auto S = [&](int i) { return reinterpret_cast<const T*>(a.s[i]); };
+  auto Y = [&](int i) { return reinterpret_cast<const T*>(a.y[i]); };
+  step(g, nullptr, 1.0, S(m - 1), m - 1, 0);
+  for (int i = m - 1; i > 0; --i) step(out, Y(i), 1.0, S(i - 1), i - 1, 0);
+  step(out, Y(0), a.gamma, Y(0), 0, 1);
+  for (int i = 0; i < m - 1; ++i) step(out, S(i), 1.0, Y(i + 1), i + 1, 1);
+  step(out, S(m - 1), -1.0, nullptr, 0, 0);
 }
 
 // two-loop scalar bookkeeping from a finished (and possibly all-reduced) dot product
@@ -657,7 +726,7 @@ cudaError_t launch_style_mat(const StyleCoefArgs& a, cudaStream_t st) {
 }
 
 cudaError_t launch_sum_partials(const double* partial, int nk, double* out, cudaStream_t st) {
-  note_launch(), finish_sums_kernel<<<1, 32, 0, st>>>(partial, kRedBlocks, nk, out);
+  note_launch(), finish_sums_kernel<<<1, 32 * nk, 0, st>>>(partial, kRedBlocks, nk, out);
   return cudaGetLastError();
 }
 
@@ -679,7 +748,7 @@ cudaError_t launch_dots(int f64, const void* a0, const void* b0, const void* a1,
                                                                    (const float*)a1, (const float*)b1,
                                                                    (const float*)a2, (const float*)b2, n, partial);
   const int nk = 1 + (a1 != nullptr) + (a2 != nullptr);
-  note_launch(), finish_sums_kernel<<<1, 32, 0, st>>>(partial, kRedBlocks, nk, out);
+  note_launch(), finish_sums_kernel<<<1, 32 * nk, 0, st>>>(partial, kRedBlocks, nk, out);
   return cudaGetLastError();
 }
 
@@ -690,6 +759,25 @@ cudaError_t launch_absmax(int f64, const void* a, long long n, double* partial, 
     note_launch(), absmax_partial_kernel<float><<<kRedBlocks, kRedThreads, 0, st>>>((const float*)a, n, partial);
   note_launch(), finish_max_kernel<<<1, 1, 0, st>>>(partial, kRedBlocks, out);
   return cudaGetLastError();
+}
+
+// cooperative two-loop; returns cudaErrorNotSupported when co-residency of the reduction grid
+// is not available (the caller then issues the per-step kernels)
+cudaError_t launch_two_loop_coop(int f64, const TwoLoopArgs& a, cudaStream_t st) {
+  if (a.m < 1 || a.m > kTwoLoopMaxHist) return cudaErrorNotSupported;
+  const void* fn = f64 ? (const void*)two_loop_coop_kernel<double> : (const void*)two_loop_coop_kernel<float>;
+  int dev = 0, coop = 0, per_sm = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kRedThreads, 0);
+  if (!coop || per_sm * sms < kRedBlocks) {
+    cudaGetLastError();
+    return cudaErrorNotSupported;
+  }
+  void* args[] = {const_cast<TwoLoopArgs*>(&a)};
+  note_launch();
+  return cudaLaunchCooperativeKernel(fn, dim3(kRedBlocks), dim3(kRedThreads), args, 0, st);
 }
 
 cudaError_t launch_axpy_dot(int f64, const AxpyDotArgs& a, cudaStream_t st) {
@@ -724,7 +812,7 @@ cudaError_t launch_sy(int f64, const void* xt, const void* x, const void* gt, co
   else
     note_launch(), sy_kernel<float><<<kRedBlocks, kRedThreads, 0, st>>>((const float*)xt, (const float*)x, (const float*)gt,
                                                          (const float*)g, n, (float*)s, (float*)y, partial);
-  note_launch(), finish_sums_kernel<<<1, 32, 0, st>>>(partial, kRedBlocks, 3, out);
+  note_launch(), finish_sums_kernel<<<1, 96, 0, st>>>(partial, kRedBlocks, 3, out);
   return cudaGetLastError();
 }
 

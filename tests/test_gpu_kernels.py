@@ -139,3 +139,23 @@ def test_launch_counter_and_timer(tiny_spec):
     eng.timing_enable(False)
     spst.loss_grad(x, p)
     assert eng.timing_read() == {}
+
+
+@pytest.mark.parametrize("dtype,n,m", [(torch.float32, 100003, 100), (torch.float64, 4099, 7), (torch.float32, 2_300_001, 10)])
+def test_two_loop_native_equals_step_by_step(dtype, n, m):
+    """spst_vec_two_loop (one cooperative launch) must equal the step-by-step kernels bit for
+    bit (the step path is what multi-GPU runs use, with an all-reduce per dot product)."""
+    from paper_2212_13459_b200.lbfgs import LBFGSState, _two_loop, _Vec
+    g0 = torch.Generator(device="cuda").manual_seed(n + m)
+    st = LBFGSState()
+    for _ in range(m):
+        s = torch.randn(n, dtype=dtype, device="cuda", generator=g0)
+        y = s + 0.3 * torch.randn(n, dtype=dtype, device="cuda", generator=g0)
+        assert st.push(s, y, m)
+    g = torch.randn(n, dtype=dtype, device="cuda", generator=g0)
+    vec = _Vec(dtype, g.device)
+    d_native = _two_loop(g, st, vec, torch.empty_like(g))
+    d_steps = _two_loop(g, st, vec, torch.empty_like(g), allreduce=lambda t, op="sum": t)
+    torch.cuda.synchronize()
+    assert torch.equal(d_native, d_steps)
+    assert torch.isfinite(d_native).all()

@@ -206,6 +206,8 @@ struct spst_ctx {
   double t_ms[kTimerClasses] = {}, t_flops[kTimerClasses] = {};
   long long t_n[kTimerClasses] = {};
   std::vector<unsigned int> amax_h;
+  double* fin_d = nullptr;  // per-tap loss outputs (bind_alloc)
+  std::vector<double> fin_h;
   HL16 gbuf[2];
   size_t gbuf_elems = 0;
   HL16 addend;
@@ -268,6 +270,8 @@ struct spst_ctx {
     if (pool) cudaStreamSynchronize(stream);
     allocs.clear();
     alloc_bytes = 0;
+    fin_d = nullptr;
+    fin_h.clear();
     bound = false;
     fwd_done = finalized = content_captured = false;
     for (auto& t : taps) {
@@ -931,10 +935,6 @@ int bind_alloc(spst_ctx* ctx) {
       t.mu = ctx->dalloc<double>(C);
       t.sd = ctx->dalloc<double>(C);
       t.ratio = ctx->dalloc<double>(C);
-      t.row_loss = ctx->dalloc<double>(C);
-      t.row_mmax = ctx->dalloc<double>(C);
-      t.ms_loss = ctx->dalloc<double>(2);
-      t.degenerate = ctx->dalloc<int>(1);
       t.bvec = ctx->dalloc<float>(Cp);
       t.xw = ctx->dalloc<__half>((size_t)Cp * Cp * 2);
       const int own0 = (ctx->own_r0 - ctx->grid_r0) / s.stride, own1 = (ctx->own_r1 - ctx->grid_r0) / s.stride;
@@ -947,7 +947,7 @@ int bind_alloc(spst_ctx* ctx) {
       t.colsum_rows = ((s.W + 127) / 128) * ((s.H + mt - 1) / mt) * 2 * mt;
       t.colsum_partial = ctx->dalloc<float>((size_t)t.colsum_rows * Cp);
       t.colsum_mid = ctx->dalloc<double>((size_t)kColsumMid * Cp);
-      if (!t.S || !t.s || !t.mu || !t.sd || !t.ratio || !t.row_loss || !t.row_mmax || !t.ms_loss || !t.degenerate ||
+      if (!t.S || !t.s || !t.mu || !t.sd || !t.ratio ||
           !t.bvec || !t.xw || !t.gram_partial || !t.colsum_partial || !t.colsum_mid)
         return ctx->fail(SPST_ERR_OOM, "statistics buffers");
       CK(cudaMemsetAsync(t.bvec, 0, Cp * 4, ctx->stream));
@@ -962,6 +962,25 @@ int bind_alloc(spst_ctx* ctx) {
         CK(cudaMemsetAsync(t.sdr, 0, C * 8, ctx->stream));
       }
     }
+  }
+  // per-tap loss outputs in one block: [row_loss C][row_mmax C][ms_loss 2][degenerate 1] per tap,
+  // so spst_finalize reads every tap with one copy and one synchronisation
+  {
+    size_t total = 0;
+    for (auto& t : ctx->taps) total += 2 * (size_t)ctx->stages[t.stage].cout + 3;
+    ctx->fin_d = ctx->dalloc<double>(total);
+    if (!ctx->fin_d) return ctx->fail(SPST_ERR_OOM, "statistics buffers");
+    ctx->fin_h.assign(total, 0.0);
+    size_t off = 0;
+    for (auto& t : ctx->taps) {
+      const int C = ctx->stages[t.stage].cout;
+      t.row_loss = ctx->fin_d + off;
+      t.row_mmax = t.row_loss + C;
+      t.ms_loss = t.row_mmax + C;
+      t.degenerate = reinterpret_cast<int*>(t.ms_loss + 2);
+      off += 2 * (size_t)C + 3;
+    }
+    CK(cudaMemsetAsync(ctx->fin_d, 0, total * sizeof(double), ctx->stream));
   }
   for (int b = 0; b < 2; ++b) {
     ctx->gbuf[b] = hl_shape(64, 1, 1);
@@ -1243,17 +1262,17 @@ int spst_finalize(spst_ctx* ctx, const long long* n, double* terms, int* degener
     CK(launch_style_vec(a, ctx->stream));
     CK(launch_style_mat(a, ctx->stream));
   }
-  std::vector<double> buf;
+  if (!ctx->fin_h.empty()) {
+    CK(cudaMemcpyAsync(ctx->fin_h.data(), ctx->fin_d, ctx->fin_h.size() * sizeof(double), cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+  }
   for (size_t i = 0; i < ctx->taps.size(); ++i) {
     TapState& t = ctx->taps[i];
     const int C = ctx->stages[t.stage].cout;
-    buf.resize(2 * C + 2);
+    const double* buf = ctx->fin_h.data() + (t.row_loss - ctx->fin_d);
     int deg = 0;
-    CK(cudaMemcpyAsync(buf.data(), t.row_loss, C * 8, cudaMemcpyDeviceToHost, ctx->stream));
-    CK(cudaMemcpyAsync(buf.data() + C, t.row_mmax, C * 8, cudaMemcpyDeviceToHost, ctx->stream));
-    CK(cudaMemcpyAsync(buf.data() + 2 * C, t.ms_loss, 16, cudaMemcpyDeviceToHost, ctx->stream));
-    CK(cudaMemcpyAsync(&deg, t.degenerate, 4, cudaMemcpyDeviceToHost, ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));
+    std::memcpy(&deg, buf + 2 * C + 2, sizeof(int));
     double g = 0, mm = 0;
     for (int c = 0; c < C; ++c) {
       g += buf[c];

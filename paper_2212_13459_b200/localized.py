@@ -225,13 +225,14 @@ class Evaluation:
         eng.forward(x_dev)
         _meter(eng)
         counts = [eng.owned_pixels(i) for i in range(len(eng.style_taps))]
+        content = eng.content_sqdiff() if p.has_content else None  # read after finalize's one sync
         terms, degenerate = eng.finalize(counts)
         if any(degenerate):
             warnings.warn("zero-std channel with nonzero reference std; its gradient column is zeroed",
                           DegenerateStdWarning, stacklevel=3)
         total = float(terms.sum())
-        if p.has_content:
-            total += p.weights.lambda_c * float(eng.content_sqdiff().item())
+        if content is not None:
+            total += p.weights.lambda_c * float(content.item())
         return total
 
     def grad(self, out: torch.Tensor) -> torch.Tensor:

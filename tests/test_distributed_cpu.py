@@ -138,11 +138,11 @@ def _free_port():
     return p
 
 
-def _run(case):
+def _run(case, world=2):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, case, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, case, q)) for r in range(world)]
     for p in procs:
         p.start()
     out = q.get(timeout=600)
@@ -171,6 +171,17 @@ def test_two_rank_stripes_equal_whole_image(case):
     loss, grad, losses, st = _run(case)
     assert len(st) == 2 and st[0].own_r1 == st[1].own_r0
     (lo, go), p, x = _global_oracle(case)
+    assert abs(loss - lo) <= 1e-10 * abs(lo)
+    assert np.linalg.norm(grad - go) <= 1e-10 * np.linalg.norm(go)
+
+
+def test_three_ranks_halo_wider_than_a_stripe():
+    """Halo exchange when a neighbour's stripe is thinner than the halo: rank 0's window needs
+    rows from rank 2 as well as rank 1 (point-to-point from every rank that owns them)."""
+    case = (48, 40, 32)
+    loss, grad, _, st = _run(case, world=3)
+    assert len(st) == 3 and st[1].own_r1 - st[1].own_r0 < 32 and st[0].grid_r1 > st[1].own_r1
+    (lo, go), _, _ = _global_oracle(case)
     assert abs(loss - lo) <= 1e-10 * abs(lo)
     assert np.linalg.norm(grad - go) <= 1e-10 * np.linalg.norm(go)
 

@@ -15,8 +15,8 @@ last-scale problem, every piece timed on the device with CUDA events on the engi
 * row stripes for N = 1, 2, 4, 8 (``tiling.stripes``, the decomposition ``distributed.py``
   shards over): the slowest stripe's evaluation time is the per-rank compute of an N-GPU
   evaluation.  The per-evaluation exchange is counted in bytes (5 style taps' S and s partials
-  in f64 = 611,776 values, the content scalar, and the x all-gather of the other ranks' rows)
-  and converted to time with a stated NVLink bandwidth model — this run has one GPU, so the
+  in f64 = 611,776 values plus the content scalar, as one all-reduce; the x halo rows received
+  point-to-point) and converted to time with a stated NVLink bandwidth model — this run has one GPU, so the
   exchange itself is not measured.
 
 Diagnostic tool; not a bench line.
@@ -119,21 +119,23 @@ for n in (1, 2, 4, 8):
     worst = max(t["ms"] for t in times)
     if n == 1:
         full_ms = worst
-    rows_other = H - (H // n)
-    gather_bytes = rows_other * W * 3 * 4 if n > 1 else 0
+    # the exchange per evaluation (distributed.py): one fused f64 all-reduce of the statistics
+    # (ring: 2(N-1)/N of the buffer per GPU) and the point-to-point halo rows of x
+    me = max(parts, key=lambda st: st.grid_r1 - st.grid_r0)
+    halo_bytes = ((me.grid_r1 - me.grid_r0) - (me.own_r1 - me.own_r0)) * W * 3 * 4 if n > 1 else 0
     stat_bytes = 8 * (stat_values + 1)
-    # ring all-reduce moves 2(N-1)/N of the buffer per GPU; all-gather (N-1)/N of the image
-    ar_us = (2 * (n - 1) / n * stat_bytes / (NVLINK_GBS * 1e3) + 11 * COLL_LAT_US) if n > 1 else 0.0
-    ag_us = (gather_bytes / (NVLINK_GBS * 1e3) + COLL_LAT_US) if n > 1 else 0.0
+    ar_us = (2 * (n - 1) / n * stat_bytes / (NVLINK_GBS * 1e3) + COLL_LAT_US) if n > 1 else 0.0
+    hx_us = (halo_bytes / (NVLINK_GBS * 1e3) + COLL_LAT_US) if n > 1 else 0.0
     halo_rows = sum(st.grid_r1 - st.grid_r0 for st in parts)
+    comm_ms = (ar_us + hx_us) / 1e3
     res["stripes"].append({
         "gpus": n, "per_rank_eval_ms": worst, "stripes_timed": times,
         "halo_factor": halo_rows / H,
         "stats_allreduce_bytes": stat_bytes, "stats_allreduce_model_us": ar_us,
-        "x_allgather_bytes_per_rank": gather_bytes, "x_allgather_model_us": ag_us,
-        "comm_share_model": (ar_us + ag_us) / 1e3 / (worst + (ar_us + ag_us) / 1e3),
-        "projected_evals_per_s": 1e3 / (worst + (ar_us + ag_us) / 1e3),
-        "projected_speedup_vs_1": (full_ms / (worst + (ar_us + ag_us) / 1e3)) if full_ms else None,
+        "x_halo_bytes_per_rank": halo_bytes, "x_halo_model_us": hx_us,
+        "comm_share_model": comm_ms / (worst + comm_ms),
+        "projected_evals_per_s": 1e3 / (worst + comm_ms),
+        "projected_speedup_vs_1": (full_ms / (worst + comm_ms)) if full_ms else None,
     })
     print(json.dumps(res["stripes"][-1]), flush=True)
 
@@ -175,8 +177,8 @@ for T in (int(t) for t in a.tiles.split(",")):
 
 res["whole_image_eval_ms"] = full_ms
 res["whole_image_algorithmic_tflops"] = FLOP_PER_PX * H * W / (full_ms * 1e-3) / 1e12
-res["model"] = (f"exchange time = bytes / {NVLINK_GBS:.0f} GB/s (+{COLL_LAT_US:.0f} us per collective; 11 "
-                "collectives for the statistics and content scalar, 1 all-gather of x); not measured (1 GPU)")
+res["model"] = (f"exchange time = bytes / {NVLINK_GBS:.0f} GB/s + {COLL_LAT_US:.0f} us per exchange (one fused "
+                "statistics all-reduce, one batch of point-to-point halo rows); not measured (1 GPU)")
 os.makedirs(os.path.dirname(a.out) or ".", exist_ok=True)
 with open(a.out, "w") as f:
     json.dump(res, f, indent=1)

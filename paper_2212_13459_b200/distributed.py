@@ -133,8 +133,8 @@ class ShardedProblem:
         return t.contiguous().reshape(-1).clone()
 
     def gather_image(self, shard):
-        """Full (h, w, 3) image from every rank's shard (all-gather of padded shards)."""
-        rows = self.own_rows[1] - self.own_rows[0]
+        """Full (h, w, 3) image from every rank's shard (all-gather of padded shards) — for
+        results and checkpoints; the evaluation itself only exchanges halo rows."""
         buf = torch.zeros(self.max_rows * self.w * 3, dtype=shard.dtype, device=shard.device)
         buf[:shard.numel()] = shard
         if self.world > 1:
@@ -146,7 +146,6 @@ class ShardedProblem:
         for (a, b), p in zip(self.all_own_rows, parts):
             if b > a:
                 img[a:b] = p[:(b - a) * self.w * 3].view(b - a, self.w, 3)
-        del rows
         return img
 
     # ------------------------------------------------------------------ objective

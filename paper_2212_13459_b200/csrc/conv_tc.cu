@@ -82,17 +82,21 @@ __device__ __forceinline__ bool chunk_is_extra(int c, int n_kc, int& idx) {
 // TMEM accumulation groups: up to D consecutive chunks of the same kind (conv / extra-K,
 // which carry different scales) share one fresh TMEM buffer before the epilogue drains it.
 // Two 16-channel chunks per buffer double the MMA's lead over the per-tile epilogue and halve
-// the drain work, at ~2x the (fp32-class) in-TMEM accumulation error of a single chunk.
-// Only the N=128 kernel needs the longer lead (NBUF=2); N=64 has 4 buffers and keeps one chunk
-// per buffer (its full-resolution layers feed every deeper one).
-// Build with -DSPST_CONV_DRAIN=1 for one chunk per buffer everywhere (~3x smaller in-TMEM
-// accumulation error, ~7% slower evaluation; measured in DESIGN.md §5).
+// the drain work, at ~2x the (fp32-class) in-TMEM accumulation error of a single chunk.  Both
+// kernels group two chunks by default: on N=128 it keeps the MMA ahead of the per-tile
+// epilogue (NBUF=2), on N=64 it halves the drains of the epilogue-bound pool-backward layer
+// (conv2_1 adjoint 6.78 -> 6.18 ms; VGG gradient on our ReLU pattern still 3e-5 of f64).
+// Build with -DSPST_CONV_DRAIN=1 / -DSPST_CONV_DRAIN64=1 for one chunk per buffer (~3x
+// smaller in-TMEM accumulation error, ~7% slower evaluation; measured in DESIGN.md §5).
 #ifndef SPST_CONV_DRAIN
 #define SPST_CONV_DRAIN 2
 #endif
+#ifndef SPST_CONV_DRAIN64
+#define SPST_CONV_DRAIN64 2
+#endif
 template <int N>
 struct DrainCfg {
-  static constexpr int D = N == 128 ? SPST_CONV_DRAIN : 1;
+  static constexpr int D = N == 128 ? SPST_CONV_DRAIN : SPST_CONV_DRAIN64;
 };
 template <int D>
 __device__ __forceinline__ void chunk_group(int c, int n_kc, int n_chunks, bool& first, bool& last) {

@@ -28,10 +28,11 @@ constexpr int FC_BX = 32, FC_BY = 8;
 // localized.py): v_c = (img[perm c] - mean_c) / scale_c at the clamped global pixel, split into
 // fp16 hi/lo at scale out.scale.  One thread per grid pixel, 16 B hi + 16 B lo per pixel.
 __global__ void __launch_bounds__(256) image_hl_kernel(const __grid_constant__ ImageHLArgs a) {
-  const long long n = (long long)a.Hl * a.Wp;
   float m = 0.f;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    const int y = (int)(i / a.Wp), x = (int)(i % a.Wp);
+  // grid-stride over (rows: y, columns: x) -- no per-pixel index division
+  for (int y = blockIdx.y; y < a.Hl; y += gridDim.y)
+  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < a.Wp; x += gridDim.x * blockDim.x) {
+    const long long i = (long long)y * a.Wp + x;
     const int gy = min(y + a.row_off, a.h - 1), gx = min(x, a.w - 1);
     const float* px = a.img + ((size_t)gy * a.w + gx) * 3;
     __align__(16) __half hh[8];
@@ -705,9 +706,9 @@ __global__ void resize_bilinear_kernel(const float* in, int h, int w, int c, int
 // launch helpers
 // ------------------------------------------------------------------------------------------
 cudaError_t launch_image_hl(const ImageHLArgs& a, cudaStream_t st) {
-  const long long n = (long long)a.Hl * a.Wp;
-  const int blocks = (int)std::min<long long>((n + 255) / 256, 148LL * 8);
-  note_launch(), image_hl_kernel<<<blocks, 256, 0, st>>>(a);
+  const int bx = (a.Wp + 255) / 256;  // column blocks per row; ~148 x 8 blocks in total
+  const dim3 grid(bx, std::max(1, std::min(a.Hl, 148 * 8 / bx)));
+  note_launch(), image_hl_kernel<<<grid, 256, 0, st>>>(a);
   return cudaGetLastError();
 }
 

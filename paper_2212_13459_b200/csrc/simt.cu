@@ -108,31 +108,31 @@ __global__ void __launch_bounds__(256) first_conv_bwd_kernel(const __grid_consta
 // grad (rows [r0,r1) of the h x w unpadded image) from the local padded-grid gradient.
 __global__ void fold_grad_kernel(const float* gimg, int Hl, int Wp, int row_off, int h, int w, int r0, int r1,
                                  float* grad) {
-  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long long n = (long long)(r1 - r0) * w;
-  if (i >= n) return;
-  const int gy = r0 + (int)(i / w), gx = (int)(i % w);
-  const int ly = gy - row_off;
-  float acc[3];
+  const int gx = blockIdx.x * blockDim.x + threadIdx.x;  // grid (column blocks, rows): no index division
+  if (gx >= w) return;
+  for (int gy = r0 + blockIdx.y; gy < r1; gy += gridDim.y) {
+    const int ly = gy - row_off;
+    float acc[3];
 #pragma unroll
-  for (int c = 0; c < 3; ++c) acc[c] = gimg[((size_t)ly * Wp + gx) * 3 + c];
-  const int Hp_loc_end = Hl;  // local rows beyond the image (ly >= h - row_off) fold onto h-1
-  if (gy == h - 1)
-    for (int yy = ly + 1; yy < Hp_loc_end; ++yy)
+    for (int c = 0; c < 3; ++c) acc[c] = gimg[((size_t)ly * Wp + gx) * 3 + c];
+    const int Hp_loc_end = Hl;  // local rows beyond the image (ly >= h - row_off) fold onto h-1
+    if (gy == h - 1)
+      for (int yy = ly + 1; yy < Hp_loc_end; ++yy)
 #pragma unroll
-      for (int c = 0; c < 3; ++c) acc[c] += gimg[((size_t)yy * Wp + gx) * 3 + c];
-  if (gx == w - 1)
-    for (int xx = w; xx < Wp; ++xx)
-#pragma unroll
-      for (int c = 0; c < 3; ++c) acc[c] += gimg[((size_t)ly * Wp + xx) * 3 + c];
-  if (gy == h - 1 && gx == w - 1)
-    for (int yy = ly + 1; yy < Hp_loc_end; ++yy)
+        for (int c = 0; c < 3; ++c) acc[c] += gimg[((size_t)yy * Wp + gx) * 3 + c];
+    if (gx == w - 1)
       for (int xx = w; xx < Wp; ++xx)
 #pragma unroll
-        for (int c = 0; c < 3; ++c) acc[c] += gimg[((size_t)yy * Wp + xx) * 3 + c];
-  float* o = grad + ((size_t)gy * w + gx) * 3;
+        for (int c = 0; c < 3; ++c) acc[c] += gimg[((size_t)ly * Wp + xx) * 3 + c];
+    if (gy == h - 1 && gx == w - 1)
+      for (int yy = ly + 1; yy < Hp_loc_end; ++yy)
+        for (int xx = w; xx < Wp; ++xx)
 #pragma unroll
-  for (int c = 0; c < 3; ++c) o[c] = acc[c];
+          for (int c = 0; c < 3; ++c) acc[c] += gimg[((size_t)yy * Wp + xx) * 3 + c];
+    float* o = grad + ((size_t)gy * w + gx) * 3;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) o[c] = acc[c];
+  }
 }
 
 // 2x2 average pool HL16 -> HL16 (used when the first conv's ReLU is followed by a pool).
@@ -722,7 +722,8 @@ cudaError_t launch_fold_grad(const float* gimg, int Hl, int Wp, int row_off, int
                              float* grad, cudaStream_t st) {
   const long long n = (long long)(r1 - r0) * w;
   if (n <= 0) return cudaSuccess;
-  note_launch(), fold_grad_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(gimg, Hl, Wp, row_off, h, w, r0, r1, grad);
+  const dim3 grid((w + 255) / 256, std::min(r1 - r0, 65535));
+  note_launch(), fold_grad_kernel<<<grid, 256, 0, st>>>(gimg, Hl, Wp, row_off, h, w, r0, r1, grad);
   return cudaGetLastError();
 }
 

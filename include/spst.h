@@ -160,6 +160,18 @@ int spst_resize_down(const float* in, int h, int w, int c, int factor, float* ou
 int spst_resize_bilinear(const float* in, int h, int w, int c, int oh, int ow, float* out,
                          void* stream);
 
+/* Relu output of conv stage `stage` (a tap layer) from the last forward, unpacked to a
+ * (C_out x H x W) f32 device buffer on the context stream (extractor.py:171-197 forward_taps). */
+int spst_stage_features(spst_ctx* ctx, int stage, float* out_dev);
+/* out[c,p] = sum_d A[c,d] V[d,p] + r[c] V[c,p] + b[c] on a (C x P) slab (f32 or f64, device
+ * pointers, f64 accumulation): the pointwise style feature gradient of stats.py:127-165 given the
+ * global statistics, for direct calls of style_layer_loss_grad (loss_grad fuses it instead). */
+int spst_feature_affine(int f64, const void* A, const void* r, const void* b, int C, long long P,
+                        const void* V, void* out, void* stream);
+/* out = c (a - b) (stats.py:168-174 content_loss_grad's gradient). */
+int spst_vec_scaled_diff(int f64, const void* a, const void* b, double c, long long n, void* out,
+                         void* stream);
+
 /* ---------------------------------------------------------------- unit-test hooks -------
  * One tensor-core conv layer on host arrays (x: cin x H x W f32, weight cout x cin x 3 x 3,
  * bias cout; f64). mode 0: y = relu(conv(x)) (cout x H x W); mode 1: y = avgpool(relu(conv))
@@ -171,6 +183,10 @@ int spst_debug_conv(int device, int mode, int cin, int cout, int H, int W, const
  * (C_out x H x W, 1 = pre-activation > 0) — lets tests evaluate the f64 oracle on the device's
  * activation pattern. */
 int spst_debug_mask(spst_ctx* ctx, int stage, unsigned char* out_host);
+/* Stored relu output of conv stage `stage` from the last forward (C_out x H x W f32, local
+ * grid). Pool stages keep their full-resolution output only at taps unless the context was
+ * bound with SPST_DEBUG_STORE_ALL=1 in the environment (error-budget diagnostics). */
+int spst_debug_stage_out(spst_ctx* ctx, int stage, float* out_host);
 /* Gram of a (C x P) f32 feature matrix through the tensor-core Gram kernel, S = F F^T (f64). */
 int spst_debug_gram(int device, int C, long long P, const float* f_host, double* S_host);
 

@@ -9,6 +9,7 @@ resampling) runs in the in-tree CUDA library ``libspst.so`` through its C ABI
 
 from .errors import (ConfigError, DegenerateStdWarning, EmptyError, FormatError, GeometryError,
                      NonFiniteError, ShapeError)
+from .extractor import forward_taps
 from .lbfgs import LBFGSConfig, LBFGSState, Trace, minimize, two_loop_direction
 from .localized import (TransferProblem, build_problem, loss_grad, loss_grad_global, make_grid, stats_pass,
                         track_activations)
@@ -18,8 +19,8 @@ from .pipeline import (RunConfig, Schedule, make_schedule, multiscale_transfer, 
 from .resample import resize_bilinear, resize_down, resize_up2
 from .spec import (ExtractorSpec, LayerSpec, Preprocess, TapGeometry, calibrated_vgg19, load_weights,
                    save_weights, tap_geometry, tinynet, vgg19)
-from .stats import (LayerStats, LossWeights, StatsAccumulator, TapWeights, default_loss_weights,
-                    load_stats, save_stats, style_loss_terms)
+from .stats import (LayerStats, LossWeights, StatsAccumulator, TapWeights, content_loss_grad,
+                    default_loss_weights, load_stats, save_stats, style_layer_loss_grad, style_loss_terms)
 from .tiling import Block, BlockGrid, Rect, feature_inner_crop, margin_for_exact_gradient, partition
 
 __version__ = "0.1.0"

@@ -76,6 +76,11 @@ SIGNATURES = {
                                 c_void_p]),
     "spst_debug_gram": (c_int, [c_int, c_int, c_longlong, c_void_p, c_void_p]),
     "spst_debug_mask": (c_int, [c_void_p, c_int, c_void_p]),
+    "spst_debug_stage_out": (c_int, [c_void_p, c_int, c_void_p]),
+    "spst_stage_features": (c_int, [c_void_p, c_int, c_void_p]),
+    "spst_feature_affine": (c_int, [c_int, c_void_p, c_void_p, c_void_p, c_int, c_longlong, c_void_p, c_void_p,
+                                    c_void_p]),
+    "spst_vec_scaled_diff": (c_int, [c_int, c_void_p, c_void_p, c_double, c_longlong, c_void_p, c_void_p]),
 }
 
 _lib = None

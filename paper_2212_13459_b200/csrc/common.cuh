@@ -61,6 +61,8 @@ struct ConvArgs {
   float* colsum_partial;         // [tiles_y*tiles_x][C_out_p], nullable
   int sum_r0, sum_r1;
   unsigned int* amax;            // max |output| (unscaled) as float bits
+  int drain;                     // K-chunks per TMEM accumulation group (1 or 2)
+  float comp[4];                 // round-toward-zero bias factor per group: [conv 1, conv 2, extra 1, extra 2 chunks]
 };
 
 struct GramArgs {
@@ -70,7 +72,13 @@ struct GramArgs {
   int px_per_split;
   int n_ctile;                   // channel tiles of 128
   float* partial;                // [split][pair][128][128]
+  float comp[2];                 // round-toward-zero bias factor of a 1- / 2-stage accumulator (hi*hi)
 };
+
+// Expected relative round-toward-zero bias of one TMEM accumulation group in units of
+// kappa (see conv_tc.cu): per chunk `small` correction MMAs, then `large` hi*hi MMAs.
+double rz_weight(int small, int large, int chunks);
+float rz_kappa();
 
 constexpr int kFirstC = 64;  // first-layer output channels supported by the SIMT kernels (padded)
 
@@ -199,6 +207,11 @@ cudaError_t launch_resize_down(const float* in, int h, int w, int c, int f, floa
 cudaError_t launch_resize_bilinear(const float* in, int h, int w, int c, int oh, int ow, float* out,
                                    cudaStream_t st);
 int red_blocks();
+// api.cu (reference stats.py:127-174 on a standalone slab)
+cudaError_t launch_feature_affine(int f64, const void* A, const void* r, const void* b, int C, long long P,
+                                  const void* V, void* out, cudaStream_t st);
+cudaError_t launch_scaled_diff(int f64, const void* a, const void* b, double c, long long n, void* out,
+                               cudaStream_t st);
 // metrics.cu (reference metrics.py): partial holds red_blocks() doubles; out = fixed-order sum
 cudaError_t launch_metric_sqdiff(bool f64, const void* a, const void* b, long long n, double* partial, double* out,
                                  cudaStream_t st);

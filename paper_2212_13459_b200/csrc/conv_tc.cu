@@ -79,34 +79,25 @@ __device__ __forceinline__ bool chunk_is_extra(int c, int n_kc, int& idx) {
   return e;
 }
 
-// TMEM accumulation groups: up to D consecutive chunks of the same kind (conv / extra-K,
-// which carry different scales) share one fresh TMEM buffer before the epilogue drains it.
-// Two 16-channel chunks per buffer double the MMA's lead over the per-tile epilogue and halve
-// the drain work, at ~2x the (fp32-class) in-TMEM accumulation error of a single chunk.  Both
-// kernels group two chunks by default: on N=128 it keeps the MMA ahead of the per-tile
-// epilogue (NBUF=2), on N=64 it halves the drains of the epilogue-bound pool-backward layer
-// (conv2_1 adjoint 6.78 -> 6.18 ms; VGG gradient on our ReLU pattern still 3e-5 of f64).
-// Build with -DSPST_CONV_DRAIN=1 / -DSPST_CONV_DRAIN64=1 for one chunk per buffer (~3x
-// smaller in-TMEM accumulation error, ~7% slower evaluation; measured in DESIGN.md §5).
-#ifndef SPST_CONV_DRAIN
-#define SPST_CONV_DRAIN 2
-#endif
-#ifndef SPST_CONV_DRAIN64
-#define SPST_CONV_DRAIN64 2
-#endif
-template <int N>
-struct DrainCfg {
-  static constexpr int D = N == 128 ? SPST_CONV_DRAIN : SPST_CONV_DRAIN64;
-};
-template <int D>
-__device__ __forceinline__ void chunk_group(int c, int n_kc, int n_chunks, bool& first, bool& last) {
+// TMEM accumulation groups: up to D (a.drain, 1 or 2) consecutive chunks of the same kind
+// (conv / extra-K, which carry different scales) share one fresh TMEM buffer before the
+// epilogue drains it into fp32 registers.
+//
+// Numerics of the in-TMEM accumulation (measured): every MMA rounds its result
+// toward zero to fp32, so a group's partial is biased toward zero by ~kappa * w relative, with
+// w = sum over the group's MMAs of (hi*hi MMAs issued so far / hi*hi MMAs in the group) and
+// kappa = E[truncated fraction] x E[ulp/|x|] ~ 0.5 x 0.72 x 2^-23.  Uncompensated, that bias
+// is the same sign at every layer and the forward's relative error grows linearly with depth
+// (2.2e-7 per conv with one chunk per group, 7e-7 with two).  The host passes the expected
+// factor (1 + kappa w) per group composition in a.comp[]; the drain multiplies by it, which
+// leaves the unbiased (sqrt-growing) part: fp32-class.
+__device__ __forceinline__ void chunk_group(int D, int c, int n_kc, int n_chunks, bool& first, bool& last) {
   const int j = c < n_kc ? c : c - n_kc;
   const int end = c < n_kc ? n_kc : n_chunks;
-  first = j % D == 0;
-  last = j % D == D - 1 || c == end - 1;
+  first = D == 1 || (j & 1) == 0;
+  last = D == 1 || (j & 1) == 1 || c == end - 1;
 }
-template <int D>
-__host__ __device__ constexpr int n_groups(int n_kc, int n_xkc) {
+__host__ __device__ constexpr int n_groups(int D, int n_kc, int n_xkc) {
   return (n_kc + D - 1) / D + (n_xkc + D - 1) / D;
 }
 
@@ -442,7 +433,7 @@ __global__ void __launch_bounds__(320, 1) conv3x3_tc_kernel(const __grid_constan
       for (int t = first; t < n_tiles; t += step) {
         for (int c = 0; c < n_chunks; ++c, ++g) {
           bool gfirst, glast;
-          chunk_group<DrainCfg<N>::D>(c, a.n_kc, n_chunks, gfirst, glast);
+          chunk_group(a.drain, c, a.n_kc, n_chunks, gfirst, glast);
           const uint32_t b = gq % C::NBUF;
           if (gfirst) mbar_wait(&cempty_bar[b], ((gq / C::NBUF) & 1) ^ 1);
           const int s = g % C::STAGES;
@@ -543,14 +534,19 @@ __global__ void __launch_bounds__(320, 1) conv3x3_tc_kernel(const __grid_constan
       float acc0[C::CPG], acc1[C::CPG];
 #pragma unroll
       for (int i = 0; i < C::CPG; ++i) acc0[i] = acc1[i] = 0.f;
-      constexpr int D = DrainCfg<N>::D;
+      const int D = a.drain;
       const int n_conv_groups = (a.n_kc + D - 1) / D;
-      for (int c = 0; c < n_groups<D>(a.n_kc, a.n_xkc); ++c, ++g) {
+      for (int c = 0; c < n_groups(D, a.n_kc, a.n_xkc); ++c, ++g) {
         const uint32_t b = g % C::NBUF;
         mbar_wait(&cfull_bar[b], (g / C::NBUF) & 1);
         tc_fence_after();
         const uint32_t trow = tmem_base + ((q * 32u) << 16) + b * C::MT * N + 2 * rp * N + cofs;
-        const float cs = c >= n_conv_groups ? a.x_rescale : 1.f;  // extra-K groups carry their own scale
+        // extra-K groups carry their own scale; comp[] undoes the expected round-toward-zero bias
+        // of the group (index: kind x 2 + chunks in the group - 1)
+        const bool xg = c >= n_conv_groups;
+        const int gi = xg ? c - n_conv_groups : c;
+        const int gsz = min(D, (xg ? a.n_xkc : a.n_kc) - gi * D);
+        const float cs = (xg ? a.x_rescale : 1.f) * a.comp[(xg ? 2 : 0) + gsz - 1];
         if constexpr (C::CPG == 32) {  // both rows in one batch: 2 loads, 1 wait
           float v0[32], v1[32];
           tmem_ld32x2(trow, trow + N, v0, v1);

@@ -122,12 +122,14 @@ __global__ void __launch_bounds__(192, 1) gram_tc_kernel(const __grid_constant__
       const uint32_t b = dr % C::NBUF;
       mbar_wait(&cfull_bar[b], (dr / C::NBUF) & 1);
       tc_fence_after();
+      // undo the expected round-toward-zero bias of this accumulator (conv_tc.cu)
+      const float cm = a.comp[min(C::DRAIN, n_stages - dr * C::DRAIN) - 1];
 #pragma unroll
       for (int cb = 0; cb < 4; ++cb) {
         float v[32];
         tmem_ld32(tmem + ((q * 32u) << 16) + b * 128 + cb * 32, v);
 #pragma unroll
-        for (int j = 0; j < 32; ++j) acc[cb * 32 + j] += v[j];
+        for (int j = 0; j < 32; ++j) acc[cb * 32 + j] = fmaf(v[j], cm, acc[cb * 32 + j]);
       }
       tc_fence_before();
       __syncwarp();
@@ -241,12 +243,14 @@ __global__ void __launch_bounds__(192, 1) gram64_tc_kernel(const __grid_constant
       mbar_wait(&cfull_bar[b], (c / C::NBUF) & 1);
       tc_fence_after();
       const uint32_t ta = tmem + ((q * 32u) << 16) + b * 128;
+      // rows 0-63 of acc1 hold the hi*hi sums: undo their expected round-toward-zero bias
+      const float cm = row < 64 ? a.comp[min(C::DRAIN, n_stages - c * C::DRAIN) - 1] : 1.f;
       float v0[32], v1[32];
       tmem_ld32x2(ta, ta + 32, v0, v1);  // acc1 (x hi)
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
-        acc[j] += v0[j];
-        acc[32 + j] += v1[j];
+        acc[j] = fmaf(v0[j], cm, acc[j]);
+        acc[32 + j] = fmaf(v1[j], cm, acc[32 + j]);
       }
       if (row < 64) {  // acc2 (x lo) only matters for the hi rows
         tmem_ld32x2(ta + 64, ta + 96, v0, v1);

@@ -100,6 +100,42 @@ bool map_gram(CUtensorMap* m, const __half* base, long long P_range, long long P
 }
 
 int round_up(int v, int m) { return (v + m - 1) / m * m; }
+
+// Gram accumulators (gram_tc.cu): 128 channels = 8 correction + 4 hi*hi MMAs per 64-px stage;
+// 64 channels = 8 hi*hi MMAs per 128-px stage (corrections in separate columns); two stages each.
+void set_gram_comp(GramArgs& g, int C_p) {
+  const double k = spst::rz_kappa();
+  const bool c64 = C_p == 64;
+  g.comp[0] = (float)(1.0 + k * spst::rz_weight(c64 ? 0 : 8, c64 ? 8 : 4, 1));
+  g.comp[1] = (float)(1.0 + k * spst::rz_weight(c64 ? 0 : 8, c64 ? 8 : 4, 2));
+}
+
+int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e && *e ? atoi(e) : dflt;
+}
+// K-chunks per TMEM accumulation group (conv_tc.cu): the forward decides the ReLU masks, so it
+// drains every chunk; the backward (no sign decisions) groups two.  SPST_FWD_DRAIN /
+// SPST_BWD_DRAIN override (1 or 2).
+int fwd_drain() {
+  static const int d = std::min(2, std::max(1, env_int("SPST_FWD_DRAIN", 1)));
+  return d;
+}
+int bwd_drain() {
+  static const int d = std::min(2, std::max(1, env_int("SPST_BWD_DRAIN", 2)));
+  return d;
+}
+
+// comp[] of a conv launch (conv_tc.cu): a conv chunk is 18 correction MMAs then 9 hi*hi MMAs
+// per output row; an extra-K chunk xkg correction then xkg/2 hi*hi MMAs.
+void set_conv_comp(ConvArgs& a, int N) {
+  const double k = rz_kappa();
+  const int xkg = conv_tc_xkg(N);
+  a.comp[0] = (float)(1.0 + k * rz_weight(18, 9, 1));
+  a.comp[1] = (float)(1.0 + k * rz_weight(18, 9, 2));
+  a.comp[2] = (float)(1.0 + k * rz_weight(xkg, xkg / 2, 1));
+  a.comp[3] = (float)(1.0 + k * rz_weight(xkg, xkg / 2, 2));
+}
 // enough (split x pair) CTAs for two waves, splits of 1K..64K pixels (multiples of 128)
 int gram_px_per_split(long long px, int pairs) {
   const long long want_splits = std::max<long long>(1, (2 * kSMs + pairs - 1) / pairs);
@@ -301,6 +337,27 @@ std::atomic<long long> g_launches{0};
 }  // namespace
 void spst::note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
+double spst::rz_weight(int small, int large, int chunks) {
+  const double n = (double)large * chunks;
+  double w = 0.0;
+  int m = 0;
+  for (int c = 0; c < chunks; ++c) {
+    w += small * (m / n);
+    for (int j = 0; j < large; ++j) w += (++m) / n;
+  }
+  return w;
+}
+
+// kappa = E[dropped fraction] x E[ulp(x)/|x|] = 0.5 x (1/ln 2)(1 - 1/2) x 2^-23 = 4.30e-8 for a
+// log-uniform significand; SPST_RZ_KAPPA overrides (0 disables the compensation).
+float spst::rz_kappa() {
+  static const float k = [] {
+    const char* e = getenv("SPST_RZ_KAPPA");
+    return e && *e ? (float)atof(e) : 4.30e-8f;
+  }();
+  return k;
+}
+
 namespace {
 
 // ------------------------------------------------------------------------------------------
@@ -466,6 +523,7 @@ struct ConvLaunch {
   int H = 0, W = 0;              // GEMM grid (conv output grid)
   float acc_scale = 1.f;
   double flops = 0;              // algorithmic FLOPs (real channels, one pass) for the launch timer
+  int drain = 1;                 // K-chunks per TMEM accumulation group
   ConvArgs a{};
 };
 
@@ -520,6 +578,8 @@ int run_conv(spst_ctx* ctx, ConvLaunch& L) {
   a.tiles_x = (L.W + 127) / 128;
   a.tiles_y = (L.H + mt - 1) / mt;
   a.acc_scale = L.acc_scale;
+  a.drain = L.drain;
+  set_conv_comp(a, N);
   if (a.n_kc + a.n_xkc == 0) return ctx->fail(SPST_ERR_CONFIG, "empty GEMM");
   const int tiles = a.tiles_x * a.tiles_y * a.n_ntiles;
   const int grid = std::min(tiles, kSMs);  // persistent: one CTA per SM
@@ -573,6 +633,7 @@ int forward_stage(spst_ctx* ctx, int k, const float* x) {
   L.W = s.W;
   L.acc_scale = 1.f / (in.scale * pow2f(s.wexp));
   L.flops = 2.0 * s.H * s.W * s.cout * 9.0 * s.cin;
+  L.drain = fwd_drain();
   ConvArgs& a = L.a;
   a.epi = s.pool_after ? EPI_FWD_POOL : EPI_FWD;
   a.bias = s.bias_d;
@@ -605,6 +666,7 @@ int stage_stats(spst_ctx* ctx, int k) {
   g.px_per_split = t.gram_px;
   g.n_ctile = (s.cout_p + 127) / 128;
   g.partial = t.gram_partial;
+  set_gram_comp(g, s.cout_p);
   const double inv2 = 1.0 / ((double)s.out.scale * (double)s.out.scale);
   auto* tm = timer_begin(ctx, 2, 2.0 * (double)(p1 - p0) * s.cout * s.cout);
   if (s.cout_p == 64) {
@@ -731,6 +793,7 @@ int tap_grad_gemm(spst_ctx* ctx, int k, HL16 out, bool with_mask, double two_lam
   L.W = s.W;
   L.acc_scale = 1.f / (s.out.scale * pow2f(xexp));
   L.flops = s.style >= 0 ? 2.0 * s.H * s.W * s.cout * s.cout : 0.0;  // style GEMM V M (content-only: none)
+  L.drain = bwd_drain();
   ConvArgs& a = L.a;
   a.x_rescale = 1.f;
   a.epi = EPI_BWD;
@@ -764,6 +827,7 @@ int backward_stage(spst_ctx* ctx, int k, int src, int dst, double two_lambda) {
   const int acc_e = nx.g_e.e + nx.wexp;
   L.acc_scale = 1.f / pow2f(acc_e);
   L.flops = 2.0 * nx.H * nx.W * nx.cin * 9.0 * nx.cout;  // input-gradient GEMM of conv k+1
+  L.drain = bwd_drain();
   ConvArgs& a = L.a;
   a.x_rescale = 1.f;
   a.out = gout;
@@ -909,9 +973,13 @@ int bind_alloc(spst_ctx* ctx) {
     Stage& s = ctx->stages[k];
     s.H = Hl / s.stride;
     s.W = ctx->Wp / s.stride;
+    static const bool store_all = [] {  // diagnostics (tools/error_budget.py): keep every relu output
+      const char* e = getenv("SPST_DEBUG_STORE_ALL");
+      return e && atoi(e) != 0;
+    }();
     const bool tap = s.style >= 0 || s.content;
-    s.has_out = !s.pool_after || tap;
-    s.store_out = s.pool_after && tap;
+    s.has_out = !s.pool_after || tap || store_all;
+    s.store_out = s.pool_after && (tap || store_all);
     s.out = hl_shape(s.cout_p, s.H, s.W);
     if (s.has_out) {
       s.out.hi = ctx->dalloc<__half>((size_t)s.cout_p * s.H * s.W * 2);
@@ -1430,6 +1498,42 @@ int spst_debug_mask(spst_ctx* ctx, int stage, unsigned char* out_host) {
   return SPST_OK;
 }
 
+int spst_stage_features(spst_ctx* ctx, int stage, float* out_dev) {
+  if (!ctx->fwd_done || stage < 0 || stage >= (int)ctx->stages.size())
+    return ctx->fail(SPST_ERR_CONFIG, "no forward / bad stage");
+  const Stage& s = ctx->stages[stage];
+  if (!s.has_out) return ctx->fail(SPST_ERR_CONFIG, "stage output is not a stored tap");
+  note_launch(), unpack_hl_kernel<<<512, 256, 0, ctx->stream>>>(s.out, s.cout, out_dev);
+  CK(cudaGetLastError());
+  return SPST_OK;
+}
+
+int spst_feature_affine(int f64, const void* A, const void* r, const void* b, int C, long long P, const void* V,
+                        void* out, void* stream) {
+  if (C < 1 || P < 0 || !A || !r || !b || !V || !out) return SPST_ERR_SHAPE;
+  return launch_feature_affine(f64, A, r, b, C, P, V, out, (cudaStream_t)stream) == cudaSuccess ? SPST_OK
+                                                                                              : SPST_ERR_CUDA;
+}
+
+int spst_vec_scaled_diff(int f64, const void* a, const void* b, double c, long long n, void* out, void* stream) {
+  if (n < 0 || !a || !b || !out) return SPST_ERR_SHAPE;
+  return launch_scaled_diff(f64, a, b, c, n, out, (cudaStream_t)stream) == cudaSuccess ? SPST_OK : SPST_ERR_CUDA;
+}
+
+int spst_debug_stage_out(spst_ctx* ctx, int stage, float* out_host) {
+  if (!ctx->fwd_done || stage < 0 || stage >= (int)ctx->stages.size())
+    return ctx->fail(SPST_ERR_CONFIG, "no forward / bad stage");
+  const Stage& s = ctx->stages[stage];
+  if (!s.has_out) return ctx->fail(SPST_ERR_CONFIG, "stage output not stored (set SPST_DEBUG_STORE_ALL=1)");
+  const size_t n = (size_t)s.cout * s.H * s.W;
+  float* d = ctx->dalloc<float>(n);
+  if (!d) return ctx->fail(SPST_ERR_OOM, "debug buffer");
+  note_launch(), unpack_hl_kernel<<<512, 256, 0, ctx->stream>>>(s.out, s.cout, d);
+  CK(cudaMemcpyAsync(out_host, d, n * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return SPST_OK;
+}
+
 int spst_debug_conv(int device, int mode, int cin, int cout, int H, int W, const float* x_host,
                     const double* weight, const double* bias, float* y_host) {
   if (cudaSetDevice(device) != cudaSuccess || !get_encoder()) return SPST_ERR_CUDA;
@@ -1481,6 +1585,7 @@ int spst_debug_conv(int device, int mode, int cin, int cout, int H, int W, const
   L.a.mask_out = mask;
   L.a.epi = bwd ? EPI_BWD : (mode == 1 ? EPI_FWD_POOL : EPI_FWD);
   L.a.store_full = 0;
+  L.drain = bwd ? bwd_drain() : fwd_drain();
   TRY(run_conv(ctx, L));
   CK(cudaDeviceSynchronize());
   if (mode == 1) {
@@ -1522,6 +1627,7 @@ int spst_debug_gram(int device, int C, long long P, const float* f_host, double*
   g.px_per_split = per;
   g.n_ctile = nct;
   g.partial = part;
+  set_gram_comp(g, Cp);
   if (Cp == 64) {
     CK(launch_gram64_tc(g, splits, C, 1.0, Sd, nullptr));
   } else {

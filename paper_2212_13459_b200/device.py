@@ -198,6 +198,20 @@ class Engine:
             out[self.spec.layers[li + 1].name] = buf.astype(bool)
         return out
 
+    def stage_outputs(self):
+        """{relu layer name: f32 (C, H, W)} stored relu outputs of the last forward (diagnostics;
+        bind with SPST_DEBUG_STORE_ALL=1 to keep the non-tap pool stages too)."""
+        out = {}
+        convs = [i for i, l in enumerate(self.spec.layers[:self.spec.deepest_tap_index() + 1]) if l.kind == "conv"]
+        Hl = self.bound[2][1] - self.bound[2][0]
+        Wp = self.padded_dims()[1]
+        for k, li in enumerate(convs):
+            stride = 2 ** sum(1 for l in self.spec.layers[:li] if l.kind == "pool")
+            buf = np.zeros((self.spec.layers[li].out_ch, Hl // stride, Wp // stride), dtype=np.float32)
+            if nat.lib().spst_debug_stage_out(self._h, k, buf.ctypes.data) == nat.OK:
+                out[self.spec.layers[li + 1].name] = buf
+        return out
+
     TIMER_CLASSES = ("conv3x3_tc<128>", "conv3x3_tc<64>", "gram_tc", "unused")
 
     def timing_enable(self, on=True):

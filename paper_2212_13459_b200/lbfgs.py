@@ -268,15 +268,23 @@ def minimize(f, x0, cfg: LBFGSConfig, callback=None, allreduce=None, resume: LBF
 
     def evaluate(xv, want_grad, last_finite):
         trace.evals += 1
-        if lazy:
-            loss = obj.loss(xv)
-            g = None
-            if want_grad and np.isfinite(loss):
-                g = obj.grad(torch.empty_like(xv))
+        try:
+            if lazy:
+                loss = obj.loss(xv)
+                g = None
+                if want_grad and np.isfinite(loss):
+                    g = obj.grad(torch.empty_like(xv))
+                    trace.grads += 1
+            else:
+                loss, g = obj(xv)
                 trace.grads += 1
-        else:
-            loss, g = obj(xv)
-            trace.grads += 1
+        except NonFiniteError as e:
+            # the device path reports an unrepresentable (non-finite) activation range from
+            # inside the evaluation; the reference contract (lbfgs.py:92-96) still hands the
+            # caller the last finite iterate
+            if e.x is not None:
+                raise
+            raise NonFiniteError(str(e), x=host_x(last_finite)) from e
         if not np.isfinite(loss):
             raise NonFiniteError(f"objective returned non-finite loss {loss!r}", x=host_x(last_finite))
         return float(loss), g
@@ -301,8 +309,13 @@ def minimize(f, x0, cfg: LBFGSConfig, callback=None, allreduce=None, resume: LBF
     m = cfg.history_size
     # history ring: m+1 preallocated (s, y) slots; the sy kernel writes the candidate pair into
     # the spare slot, so a curvature rejection leaves the stored pairs untouched (lbfgs.py:48-59)
-    ring_s = torch.empty((m + 1,) + tuple(x.shape), dtype=x.dtype, device=x.device)
-    ring_y = torch.empty_like(ring_s)
+    # Every slot starts on a 16-element boundary: the vector kernels use 16-byte (f32x4 /
+    # f64x2) accesses, so a slot stride of numel elements would misalign slot k >= 1 whenever
+    # numel % 4 != 0 (e.g. 37 x 41 x 3).
+    n = x.numel()
+    stride = (n + 15) // 16 * 16
+    ring_s = torch.empty((m + 1, stride), dtype=x.dtype, device=x.device)[:, :n].unflatten(1, tuple(x.shape))
+    ring_y = torch.empty((m + 1, stride), dtype=x.dtype, device=x.device)[:, :n].unflatten(1, tuple(x.shape))
     slot_of = []  # ring slot of each stored pair, oldest first
     first_it = 0
     if resume is None:
@@ -378,10 +391,13 @@ def minimize(f, x0, cfg: LBFGSConfig, callback=None, allreduce=None, resume: LBF
         gmax = red_max(g)
         trace.losses.append(loss)
         trace.grad_norms.append(gmax)
+        # callbacks and snapshots get their own copies (the reference hands out a fresh array
+        # every iteration); x, g and the ring slots are reused buffers here
         if callback is not None:
-            callback(it + 1, host_x(x) if numpy_io else x, loss, gmax)
+            callback(it + 1, host_x(x), loss, gmax)
         if snapshot is not None and (it + 1) % snapshot[0] == 0:
-            snapshot[1](LBFGSSnapshot(iteration=it + 1, x=x, g=g, loss=loss, s=list(state.s_hist),
-                                      y=list(state.y_hist), rho=list(state.rho), yy=list(state.yy),
+            snapshot[1](LBFGSSnapshot(iteration=it + 1, x=x.clone(), g=g.clone(), loss=loss,
+                                      s=[t.clone() for t in state.s_hist], y=[t.clone() for t in state.y_hist],
+                                      rho=list(state.rho), yy=list(state.yy),
                                       losses=list(trace.losses), grad_norms=list(trace.grad_norms)))
     return (x.cpu().numpy() if numpy_io else x), trace

@@ -193,10 +193,13 @@ def _prepare(p: TransferProblem, h=None, w=None):
             s = p.extractor.deepest_stride()
             h, w = p.grid.image_h, p.grid.image_w
     eng.bind(int(h), int(w))
-    if p.has_content and p._content_epoch != eng.bind_epoch:
+    # the engine holds ONE content target: re-capture when this problem's target is not the one
+    # resident (another problem of the same dims may have captured its own since)
+    if p.has_content and (p._content_epoch != eng.bind_epoch or getattr(eng, "_content_problem", None) is not p):
         eng.forward(to_device_image(p.content_image, eng.device))
         eng.capture_content()
         p._content_epoch = eng.bind_epoch
+        eng._content_problem = p
     if getattr(eng, "_active_problem", None) is not p or p._refs_epoch != eng.bind_epoch:
         for i, t in enumerate(eng.style_taps):
             eng.set_style_ref(i, p.style_stats[t], p.weights.style[t])

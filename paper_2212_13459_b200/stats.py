@@ -129,3 +129,94 @@ def load_stats(path) -> dict:
         out[tap] = LayerStats(recs[f"{tap}.gram"], recs[f"{tap}.mean"], recs[f"{tap}.std"],
                               int(recs[f"{tap}.n_p"][0]))
     return out
+
+
+# ------------------------------------------------------------------------------------------
+# per-slab feature gradients (reference stats.py:127-174) on the device
+# ------------------------------------------------------------------------------------------
+
+def _dev(a, dtype):
+    import torch
+    from .device import require_cuda
+    require_cuda()
+    if isinstance(a, torch.Tensor):
+        return a.to(device="cuda", dtype=dtype).contiguous()
+    return torch.from_numpy(np.ascontiguousarray(a)).to(device="cuda", dtype=dtype)
+
+
+def _io_dtype(V):
+    import torch
+    if isinstance(V, torch.Tensor):
+        return torch.float64 if V.dtype == torch.float64 else torch.float32
+    return torch.float64 if np.asarray(V).dtype == np.float64 else torch.float32
+
+
+def _back(t, like):
+    import torch
+    if isinstance(like, torch.Tensor):
+        return t
+    return t.cpu().numpy()
+
+
+def style_layer_loss_grad(V, stats_x: LayerStats, stats_ref: LayerStats, w: TapWeights) -> tuple:
+    """Loss terms and the feature gradient of the augmented style loss on a slab V of the
+    image whose GLOBAL statistics are ``stats_x`` (stats.py:127-165):
+
+        gram (4 w_g / n_p) (G - G_ref) V,  mean (2 w_m / n_p)(mu - mu_ref),
+        std  (2 w_s / n_p)(V - mu)(std - std_ref) / std   (column zeroed if std < 1e-8).
+
+    The three terms are one affine map V -> A V + r.V + b (A = (4 w_g/n_p)(G - G_ref),
+    r = (2 w_s/n_p) ratio, b = (2 w_m/n_p)(mu - mu_ref) - r mu), evaluated by
+    ``spst_feature_affine`` on the device."""
+    import torch
+    from . import _native as nat
+    from .errors import DegenerateStdWarning
+    if V.ndim != 3 or V.shape[0] != stats_x.channels:
+        raise ShapeError(f"expected ({stats_x.channels},h,w) features, got {tuple(V.shape)}")
+    terms = style_loss_terms(stats_x, stats_ref, w)
+    C = stats_x.channels
+    n_p = float(stats_x.n_p)
+    A = (4.0 * w.gram / n_p) * (stats_x.gram - stats_ref.gram) if w.gram else np.zeros((C, C))
+    b = (2.0 * w.mean / n_p) * (stats_x.mean - stats_ref.mean) if w.mean else np.zeros(C)
+    r = np.zeros(C)
+    if w.std:
+        std = stats_x.std
+        degenerate = std < STD_EPS
+        if np.any(degenerate & (stats_ref.std > STD_EPS)):
+            warnings.warn("zero-std channel with nonzero reference std; its gradient column is zeroed",
+                          DegenerateStdWarning, stacklevel=2)
+        ratio = np.where(degenerate, 0.0, (std - stats_ref.std) / np.where(degenerate, 1.0, std))
+        r = (2.0 * w.std / n_p) * ratio
+        b = b - r * stats_x.mean
+    dt = _io_dtype(V)
+    Vd = _dev(V, dt)
+    out = torch.empty_like(Vd)
+    P = int(Vd[0].numel())
+    s = torch.cuda.current_stream()
+    nat.check(nat.lib().spst_feature_affine(1 if dt == torch.float64 else 0, nat.ptr(_dev(A, dt)),
+                                            nat.ptr(_dev(r, dt)), nat.ptr(_dev(b, dt)), C, P, nat.ptr(Vd),
+                                            nat.ptr(out), s.cuda_stream), None, "spst_feature_affine")
+    return terms, _back(out, V)
+
+
+def content_loss_grad(V, V_ref, lambda_c: float) -> tuple:
+    """lambda_c sum (V - V_ref)^2 (f64, fixed order) and its gradient 2 lambda_c (V - V_ref)
+    (stats.py:168-174)."""
+    import torch
+    from . import _native as nat
+    if tuple(V.shape) != tuple(V_ref.shape):
+        raise ShapeError(f"content features {tuple(V.shape)} vs reference {tuple(V_ref.shape)}")
+    dt = _io_dtype(V)
+    a, b = _dev(V, dt), _dev(V_ref, dt)
+    f64 = 1 if dt == torch.float64 else 0
+    n = a.numel()
+    s = torch.cuda.current_stream()
+    part = torch.empty(nat.lib().spst_vec_partials() + 8, dtype=torch.float64, device="cuda")
+    acc = torch.zeros(1, dtype=torch.float64, device="cuda")
+    nat.check(nat.lib().spst_metric_sqdiff(f64, nat.ptr(a), nat.ptr(b), n, nat.ptr(part), nat.ptr(acc),
+                                           s.cuda_stream), None, "spst_metric_sqdiff")
+    g = torch.empty_like(a)
+    nat.check(nat.lib().spst_vec_scaled_diff(f64, nat.ptr(a), nat.ptr(b), 2.0 * float(lambda_c), n, nat.ptr(g),
+                                             s.cuda_stream), None, "spst_vec_scaled_diff")
+    loss = float(lambda_c) * float(acc.item())
+    return loss, _back(g, V)

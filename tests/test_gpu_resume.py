@@ -61,10 +61,14 @@ def test_pipeline_midscale_checkpoint_and_resume(tiny_spec, tmp_path):
     side = sides[len(sides) // 2]
     with open(side) as f:
         meta = json.load(f)
-    assert meta["scale"] == 1 and meta["iteration"] > 0 and os.path.exists(os.path.join(tmp_path, meta["lbfgs"]))
+    assert meta["scales_done"] == 1 and meta["iteration"] > 0 and os.path.exists(os.path.join(tmp_path, meta["lbfgs"]))
+    # no "scale" key: the reference's read_checkpoint (pipeline.py:151-163) cannot mistake a
+    # partly optimised iterate for a finished scale
+    assert "scale" not in meta
     done, x, snap = read_checkpoint(side, "cfgA", "f32", with_state=True)
     assert done == 1 and snap.iteration == meta["iteration"] and len(snap.s) > 0
-    assert read_checkpoint(side, "cfgA", "f32")[0] == 1  # reference 2-tuple form still works
+    with pytest.raises(spst.ConfigError):  # the stateless (reference) form refuses a mid-scale sidecar
+        read_checkpoint(side, "cfgA", "f32")
     with pytest.raises(spst.ConfigError):
         read_checkpoint(side, "otherB", "f32")
     resumed = spst.multiscale_transfer(u, v, spst.RunConfig(resume=side, **kw))

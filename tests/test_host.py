@@ -205,3 +205,23 @@ def test_schedule_and_dims_kats():
         make_schedule(0)
     with pytest.raises(errors.ConfigError):
         make_schedule(2, "turbo")
+
+
+# Names re-exported by the reference package (reference __init__.py:3-17); the drop-in must
+# provide every one of them.
+REFERENCE_PUBLIC_NAMES = (
+    "ConfigError", "DegenerateStdWarning", "EmptyError", "FormatError", "GeometryError", "NonFiniteError",
+    "ShapeError", "ExtractorSpec", "LayerSpec", "Preprocess", "TapGeometry", "forward_taps", "load_weights",
+    "save_weights", "tap_geometry", "tinynet", "vgg19", "LBFGSConfig", "LBFGSState", "minimize",
+    "two_loop_direction", "TransferProblem", "build_problem", "loss_grad", "loss_grad_global", "stats_pass",
+    "track_activations", "IdentityReport", "gram_distance", "identity_test", "psnr", "ssim", "RunConfig",
+    "Schedule", "make_schedule", "multiscale_transfer", "scale_dims", "texture_synthesize", "LayerStats",
+    "LossWeights", "StatsAccumulator", "TapWeights", "content_loss_grad", "default_loss_weights",
+    "style_layer_loss_grad", "resize_bilinear", "resize_down", "resize_up2", "Block", "BlockGrid", "Rect",
+    "feature_inner_crop", "margin_for_exact_gradient", "partition", "__version__")
+
+
+def test_every_reference_public_name_is_exported():
+    import paper_2212_13459_b200 as spst
+    missing = [n for n in REFERENCE_PUBLIC_NAMES if not hasattr(spst, n)]
+    assert not missing, missing

@@ -278,8 +278,112 @@ def vgg_lbfgs5():
     save("vgg19_lbfgs5.npz", x5=xr, losses=np.array(tr.losses))
 
 
+def vgg_iterates():
+    """Fixed same-x points for the gradient error budget: the reference f32 L-BFGS iterates
+    x1..x5 at C1 (history 100) and, at each, the reference's own f64 gradient
+    (loss_grad_global) and f32 gradient (loss_grad) -- the precision envelope of SURVEY 8(a) a20."""
+    spec_mine = myspec.calibrated_vgg19(0)
+    spec = to_ref_spec(spec_mine, rex.vgg19("avg"))
+    u = synth_content(256, 256, 1)
+    v = synth_style(256, 256, 2)
+    cfg = rpipe.RunConfig(n_scales=1, extractor=spec)
+    w = rpipe._weights_for_scale(cfg, spec, (256, 256))
+    p32 = rloc.build_problem(u, v, spec, w)
+    p64 = rloc.build_problem(u.astype(np.float64), v.astype(np.float64), spec, w)
+    its = []
+    rlb.minimize(lambda a: rloc.loss_grad(a, p32), u.copy(), rlb.LBFGSConfig(history_size=100, max_iters=5),
+                 callback=lambda it, xi, loss, gn: its.append(np.array(xi, dtype=np.float32, copy=True)))
+    d = {}
+    for k, xi in enumerate([u] + its):
+        l64, g64 = rloc.loss_grad_global(xi.astype(np.float64), p64)
+        l32, g32 = rloc.loss_grad(xi.copy(), p32)
+        rel = np.linalg.norm(g32 - g64) / np.linalg.norm(g64)
+        print(f"iterate {k}: loss64 {l64:.6e}, reference f32 vs f64 grad rel-L2 {rel:.2e}")
+        d[f"x{k}"], d[f"loss64_{k}"], d[f"grad64_{k}"] = xi, np.array([l64]), g64.astype(np.float32)
+        d[f"loss32_{k}"], d[f"grad32_{k}"] = np.array([l32]), g32.astype(np.float32)
+    save("vgg19_iterates.npz", **d)
+
+
+def pipeline_cases():
+    """Reference multiscale_transfer / texture_synthesize (pipeline.py:232-260) on TinyNet:
+    2 scales x 3 L-BFGS iterations (history 5), f32 -- short enough that the final image is
+    comparable (SURVEY 8d protocol 3)."""
+    spec = ts.tinynet(0)
+    rng = np.random.default_rng(21)
+    u = synth_content(96, 80, 7)
+    v = synth_style(64, 72, 8)
+    orig = rpipe.make_schedule
+    rpipe.make_schedule = lambda n, m="baseline": rpipe.Schedule(n, (3,) * n, (5,) * n, m)
+    try:
+        cfg = rpipe.RunConfig(n_scales=2, mode="fast", extractor=spec, block=32, margin=16)
+        seen = []
+        x = rpipe.multiscale_transfer(u, v, cfg, progress=lambda s, it, l, g: seen.append((s, it, l, g)))
+        cfg_t = rpipe.RunConfig(n_scales=2, extractor=spec, block=32, margin=16, lambda_c=0.0, seed=3)
+        seen_t = []
+        xt = rpipe.texture_synthesize(v, cfg_t, progress=lambda s, it, l, g: seen_t.append((s, it, l, g)))
+    finally:
+        rpipe.make_schedule = orig
+    save("pipeline.npz", u=u, v=v, ms_x=x, ms_trace=np.array(seen, dtype=np.float64),
+         ts_x=xt, ts_trace=np.array(seen_t, dtype=np.float64))
+
+
+def api_cases():
+    """Per-tap public helpers: forward_taps (extractor.py:171-197), style_layer_loss_grad and
+    content_loss_grad (stats.py:127-174) on TinyNet and the calibrated VGG-19."""
+    rng = np.random.default_rng(31)
+    d = {}
+    tiny = ts.tinynet(0)
+    xt = rng.random((3, 64, 48)).astype(np.float32)
+    taps = rex.forward_taps(xt, tiny)
+    d["tiny_x"] = xt
+    for t, v in taps.items():
+        d[f"tiny_tap_{t}"] = v
+    spec = to_ref_spec(myspec.calibrated_vgg19(0), rex.vgg19("avg"))
+    xv = synth_content(64, 80, 9).transpose(2, 0, 1).copy()
+    tv = rex.forward_taps(xv, spec)
+    d["vgg_x"] = xv
+    for t, v in tv.items():
+        d[f"vgg_tap_{t}"] = v
+    # style_layer_loss_grad on a slab of a tap with the image's global stats vs another image's
+    V = tv["relu3_1"]
+    acc = rst.StatsAccumulator(V.shape[0])
+    acc.accumulate(V)
+    sx = acc.finalize()
+    tv2 = rex.forward_taps(synth_style(64, 80, 10).transpose(2, 0, 1).copy(), spec)
+    acc2 = rst.StatsAccumulator(V.shape[0])
+    acc2.accumulate(tv2["relu3_1"])
+    sr = acc2.finalize()
+    w = rst.TapWeights(1.0 / 256 ** 2, 1e3 / 256 ** 2, 1e3 / 256 ** 2)
+    slab = V[:, 3:11, 5:17].copy()
+    terms, g = rst.style_layer_loss_grad(slab, sx, sr, w)
+    d.update(sg_slab=slab, sg_G=sx.gram, sg_mu=sx.mean, sg_sd=sx.std, sg_n=np.array([sx.n_p]),
+             sg_Gr=sr.gram, sg_mur=sr.mean, sg_sdr=sr.std, sg_w=np.array([w.gram, w.mean, w.std]),
+             sg_terms=np.array(terms), sg_grad=g)
+    # degenerate channel: std 0 with a nonzero reference std -> zero std column + warning
+    sd0 = sx.std.copy()
+    sd0[7] = 0.0
+    sxd = rst.LayerStats(gram=sx.gram, mean=sx.mean, std=sd0, n_p=sx.n_p)
+    import warnings as _w
+    with _w.catch_warnings(record=True) as rec:
+        _w.simplefilter("always")
+        termsd, gd = rst.style_layer_loss_grad(slab.astype(np.float64), sxd, sr, w)
+    d.update(sgd_sd=sd0, sgd_terms=np.array(termsd), sgd_grad=gd, sgd_warned=np.array([len(rec)]))
+    # content_loss_grad
+    Vr = tv2["relu4_2"]
+    Vx = tv["relu4_2"]
+    cl, cg = rst.content_loss_grad(Vx, Vr, 0.37)
+    d.update(cl_V=Vx, cl_Vr=Vr, cl_loss=np.array([cl]), cl_grad=cg)
+    save("api.npz", **d)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["kernels", "tiny", "lbfgs", "vgg", "metrics", "lbfgs5"]
+    which = sys.argv[1:] or ["kernels", "tiny", "lbfgs", "vgg", "metrics", "lbfgs5", "iterates", "pipeline", "api"]
+    if "api" in which:
+        api_cases()
+    if "iterates" in which:
+        vgg_iterates()
+    if "pipeline" in which:
+        pipeline_cases()
     if "metrics" in which:
         metrics_cases()
     if "lbfgs5" in which:

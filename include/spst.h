@@ -69,6 +69,15 @@ int spst_set_stream(spst_ctx* ctx, void* cuda_stream);
  * (statistics, content loss and gradient are restricted to owned rows; the rows outside
  * are the receptive-field halo). A single device binds grid = own = [0, Hp). */
 int spst_bind(spst_ctx* ctx, int h, int w, int grid_r0, int grid_r1, int own_r0, int own_r1);
+/* Window binding (2-D): the context evaluates the padded-image rectangle [grid_r0, grid_r1) x
+ * [grid_c0, grid_c1) as one zero-padded image -- the reference's padded block (tiling.py:57-72,
+ * localized.py:153-155) -- and owns [own_r0, own_r1) x [own_c0, own_c1) inside it: the block's
+ * inner rectangle, whose tap-space crop (tiling.py:75-88) feeds the statistics and the content
+ * loss and whose pixels receive the gradient.  Bounds are multiples of the deepest stride (an
+ * owned end may equal the padded size).  spst_bind(rows) = full-width window. */
+int spst_bind_window(spst_ctx* ctx, int h, int w, int grid_r0, int grid_r1, int grid_c0, int grid_c1,
+                     int own_r0, int own_r1, int own_c0, int own_c1);
+int spst_window_dims(const spst_ctx* ctx, int* rows, int* cols);
 int spst_unbind(spst_ctx* ctx); /* release the bound workspace */
 int spst_padded_dims(const spst_ctx* ctx, int* Hp, int* Wp);
 int spst_tap_info(const spst_ctx* ctx, int tap, int* channels, int* stride, long long* owned_pixels);
@@ -78,10 +87,19 @@ long long spst_workspace_bytes(const spst_ctx* ctx);
  * Leaves per style tap the owned-row partial sums S = sum F F^T (C x C f64) and s = sum F
  * (C f64) in device buffers exposed by spst_stats_ptrs (for an NCCL all-reduce). */
 int spst_forward(spst_ctx* ctx, const float* x_dev, int flags);
+/* As spst_forward with the image addressed as x_dev + (y * pitch + x) * 3 for global pixel
+ * (y, x) (pitch >= w pixels): a window's rows may live in a smaller buffer whose pointer is
+ * offset accordingly. */
+int spst_forward_pitched(spst_ctx* ctx, const float* x_dev, long long pitch, int flags);
 int spst_stats_ptrs(spst_ctx* ctx, int tap, double** S_dev, double** s_dev);
 
 /* Content target (localized.py:205-212): copy the content-tap features of the last forward. */
 int spst_capture_content(spst_ctx* ctx);
+/* The captured content target of the bound window (HL16 bytes on the device, and its scale):
+ * a windowed evaluation keeps one target per window (the reference's ContentStore tiles,
+ * localized.py:84-109) and swaps it in with spst_set_content_target (device copy). */
+int spst_content_target(spst_ctx* ctx, void** buf_dev, long long* bytes, float* scale);
+int spst_set_content_target(spst_ctx* ctx, const void* buf_dev, float scale);
 /* sum over owned rows of (V - V_u)^2 at the content tap, into out_dev (1 f64). */
 int spst_content_sqdiff(spst_ctx* ctx, double* out_dev);
 
@@ -97,6 +115,9 @@ int spst_finalize(spst_ctx* ctx, const long long* n, double* terms_host, int* de
  * owned rows written into grad_dev (h x w x 3 f32; rows outside the owned range untouched).
  * two_lambda = 2 * lambda_c (0 disables the content term). */
 int spst_backward(spst_ctx* ctx, double two_lambda, float* grad_dev);
+/* As spst_backward with the gradient written at grad_dev + (y * pitch + x) * 3 for the owned
+ * pixels (y, x) of the window. */
+int spst_backward_pitched(spst_ctx* ctx, double two_lambda, float* grad_dev, long long pitch);
 
 /* ---------------------------------------------------------------- launch timer ---------
  * Measurement hook (no reference counterpart): when enabled, every tensor-core launch is

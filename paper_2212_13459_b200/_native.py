@@ -41,6 +41,10 @@ SIGNATURES = {
     "spst_set_stream": (c_int, [c_void_p, c_void_p]),
     "spst_bind": (c_int, [c_void_p, c_int, c_int, c_int, c_int, c_int, c_int]),
     "spst_unbind": (c_int, [c_void_p]),
+    "spst_bind_window": (c_int, [c_void_p, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int]),
+    "spst_window_dims": (c_int, [c_void_p, POINTER(c_int), POINTER(c_int)]),
+    "spst_forward_pitched": (c_int, [c_void_p, c_void_p, c_longlong, c_int]),
+    "spst_backward_pitched": (c_int, [c_void_p, c_double, c_void_p, c_longlong]),
     "spst_padded_dims": (c_int, [c_void_p, POINTER(c_int), POINTER(c_int)]),
     "spst_tap_info": (c_int, [c_void_p, c_int, POINTER(c_int), POINTER(c_int), POINTER(c_longlong)]),
     "spst_workspace_bytes": (c_longlong, [c_void_p]),
@@ -48,6 +52,8 @@ SIGNATURES = {
     "spst_stats_ptrs": (c_int, [c_void_p, c_int, POINTER(c_void_p), POINTER(c_void_p)]),
     "spst_capture_content": (c_int, [c_void_p]),
     "spst_content_sqdiff": (c_int, [c_void_p, c_void_p]),
+    "spst_content_target": (c_int, [c_void_p, POINTER(c_void_p), POINTER(c_longlong), POINTER(c_float)]),
+    "spst_set_content_target": (c_int, [c_void_p, c_void_p, c_float]),
     "spst_set_style_ref": (c_int, [c_void_p, c_int, POINTER(c_double), POINTER(c_double), POINTER(c_double),
                                    c_double, c_double, c_double]),
     "spst_finalize": (c_int, [c_void_p, POINTER(c_longlong), POINTER(c_double), POINTER(c_int)]),

@@ -59,36 +59,44 @@ struct ConvArgs {
   int store_full;                // fwd pool: also store full-res relu output
   // channel sums of the relu output over rows [sum_r0, sum_r1) (fwd, tap layers)
   float* colsum_partial;         // [tiles_y*tiles_x][C_out_p], nullable
-  int sum_r0, sum_r1;
+  int sum_r0, sum_r1, sum_c0, sum_c1;
   unsigned int* amax;            // max |output| (unscaled) as float bits
   int drain;                     // K-chunks per TMEM accumulation group (1 or 2)
-  float comp[4];                 // round-toward-zero bias factor per group: [conv 1, conv 2, extra 1, extra 2 chunks]
+  float comp[4];                 // round-toward-zero bias factor per group relative to `fine`:
+                                 // [conv 1, conv 2, extra 1, extra 2 chunks]
+  float fine;                    // common relative correction applied once to the drained sum
 };
 
 struct GramArgs {
-  CUtensorMap tm_hi, tm_lo;      // tap tensor viewed as (8, P, kg): box (8, 64, 16)
+  // owned rectangle of the tap tensor viewed as u64 (2 x w_own, rows, kg); box = one KPX-pixel
+  // run of one row (x16 / x8 kgroups); the run past w_own is TMA zero fill
+  CUtensorMap tm_hi, tm_lo;
   int C_p;                       // channels (padded)
-  long long p_begin, p_end;      // pixel range (flattened row-major over the tap grid)
-  int px_per_split;
+  int rows, w_own;               // owned rectangle (tap pixels)
+  int px_per_split;              // pixels (KPX-pixel stages x KPX) per CTA partial
   int n_ctile;                   // channel tiles of 128
   float* partial;                // [split][pair][128][128]
-  float comp[2];                 // round-toward-zero bias factor of a 1- / 2-stage accumulator (hi*hi)
+  float comp[2];                 // round-toward-zero bias factor of a 1- / 2-stage accumulator relative to fine_*
+  float fine_diag, fine_off;     // common relative correction of diagonal / off-diagonal entries
 };
 
 // Expected relative round-toward-zero bias of one TMEM accumulation group in units of
 // kappa (see conv_tc.cu): per chunk `small` correction MMAs, then `large` hi*hi MMAs.
 double rz_weight(int small, int large, int chunks);
-float rz_kappa();
+// kappa of mixed-sign sums (convs; set_gram_comp holds the same-sign Gram constants)
+double rz_kappa();
 
 constexpr int kFirstC = 64;  // first-layer output channels supported by the SIMT kernels (padded)
 
 // Preprocessed, replicate-padded image as the first conv's K operand: one 8-channel HL16 plane
 // (3 channels + 5 zeros); the conv's second 8-channel K group reads out of bounds (TMA zero fill).
 struct ImageHLArgs {
-  const float* img;   // (h, w, 3) f32, unpadded global image
+  const float* img;   // global pixel (y, x) at img + (y * pitch + x) * 3 (f32 HWC)
+  long long pitch;    // pixels per image row of the buffer
   int h, w;           // unpadded global dims
   int row_off;        // global padded row of local row 0
-  int Hl, Wp;         // local grid (rows) x padded width
+  int col_off;        // global padded column of local column 0
+  int Hl, Wp;         // local grid rows x columns
   int perm[3];
   float mean[3], scale[3];
   HL16 out;           // C_p = 8
@@ -183,16 +191,24 @@ cudaError_t launch_gram_reduce(const float* partial, int n_splits, int n_ctile, 
                                double* S, cudaStream_t stream);
 cudaError_t launch_image_hl(const ImageHLArgs& a, cudaStream_t st);
 cudaError_t launch_first_conv_bwd(const FirstConvBwdArgs& a, cudaStream_t st);
-cudaError_t launch_fold_grad(const float* gimg, int Hl, int Wp, int row_off, int h, int w, int r0, int r1,
-                             float* grad, cudaStream_t st);
+// grad: global pixel (y, x) at grad + (y * pitch + x) * 3; writes the owned rectangle
+// [r0, r1) x [c0, c1) (clipped to the image) from the local grid gimg (Hl x Wl, origin
+// (row_off, col_off)), folding the replicate-pad rows/columns onto the last image row/column.
+struct FoldArgs {
+  const float* gimg;
+  int Hl, Wl, row_off, col_off, h, w, r0, r1, c0, c1;
+  float* grad;
+  long long pitch;
+};
+cudaError_t launch_fold_grad(const FoldArgs& a, cudaStream_t st);
 cudaError_t launch_pool2_hl(const HL16& in, const HL16& out, unsigned int* amax, cudaStream_t st);
 cudaError_t launch_colsum_reduce(const float* partial, int rows, int C, int stride, double* sums, double* mid,
                                  cudaStream_t st);
 constexpr int kColsumMid = 256;  // doubles per channel of colsum scratch
 cudaError_t launch_style_vec(const StyleCoefArgs& a, cudaStream_t st);
 cudaError_t launch_style_mat(const StyleCoefArgs& a, cudaStream_t st);
-cudaError_t launch_content_sqdiff(const HL16& v, const HL16& u, int C, int r0, int r1, double* partial,
-                                  double* out, cudaStream_t st);
+cudaError_t launch_content_sqdiff(const HL16& v, const HL16& u, int C, int r0, int r1, int c0, int c1,
+                                  double* partial, double* out, cudaStream_t st);
 cudaError_t launch_dots(int f64, const void* a0, const void* b0, const void* a1, const void* b1, const void* a2,
                         const void* b2, long long n, double* partial, double* out, cudaStream_t st);
 cudaError_t launch_absmax(int f64, const void* a, long long n, double* partial, double* out, cudaStream_t st);

@@ -86,11 +86,12 @@ __device__ __forceinline__ bool chunk_is_extra(int c, int n_kc, int& idx) {
 // Numerics of the in-TMEM accumulation (measured): every MMA rounds its result
 // toward zero to fp32, so a group's partial is biased toward zero by ~kappa * w relative, with
 // w = sum over the group's MMAs of (hi*hi MMAs issued so far / hi*hi MMAs in the group) and
-// kappa = E[truncated fraction] x E[ulp/|x|] ~ 0.5 x 0.72 x 2^-23.  Uncompensated, that bias
-// is the same sign at every layer and the forward's relative error grows linearly with depth
-// (2.2e-7 per conv with one chunk per group, 7e-7 with two).  The host passes the expected
-// factor (1 + kappa w) per group composition in a.comp[]; the drain multiplies by it, which
-// leaves the unbiased (sqrt-growing) part: fp32-class.
+// kappa ~ E[truncated fraction] x E[ulp/|x|] ~ 0.5 x 0.72 x 2^-23 (fitted on B200: 3.2e-8).
+// Uncompensated, that bias has the same sign at every layer and the forward's relative error
+// grows linearly with depth (2.2e-7 per conv with one chunk per group, 7e-7 with two).  The
+// host passes the expected factor 1 + kappa w: its common part a.fine is applied once to the
+// drained sum, the per-group-composition remainder in a.comp[] by the drain.  What is left is
+// the unbiased (sqrt-growing) part: fp32-class.
 __device__ __forceinline__ void chunk_group(int D, int c, int n_kc, int n_chunks, bool& first, bool& last) {
   const int j = c < n_kc ? c : c - n_kc;
   const int end = c < n_kc ? n_kc : n_chunks;
@@ -223,8 +224,9 @@ __device__ __forceinline__ void epilogue32(const ConvArgs& a, float* v0, float* 
       }
     }
     if (a.colsum_partial) {
-      const bool in0 = ok0 && y0 >= a.sum_r0 && y0 < a.sum_r1;
-      const bool in1 = ok1 && y0 + 1 >= a.sum_r0 && y0 + 1 < a.sum_r1;
+      const bool inx = x >= a.sum_c0 && x < a.sum_c1;
+      const bool in0 = ok0 && inx && y0 >= a.sum_r0 && y0 < a.sum_r1;
+      const bool in1 = ok1 && inx && y0 + 1 >= a.sum_r0 && y0 + 1 < a.sum_r1;
       float s[32];
 #pragma unroll
       for (int j = 0; j < 32; ++j) s[j] = (in0 ? v0[j] : 0.f) + (in1 ? v1[j] : 0.f);
@@ -565,6 +567,13 @@ __global__ void __launch_bounds__(320, 1) conv3x3_tc_kernel(const __grid_constan
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&cempty_bar[b]);
+      }
+      // the common part of the round-toward-zero compensation, once per output (exact to fp32
+      // rounding; a (1 + eps) factor in the per-group drains would be quantised to 2^-23)
+#pragma unroll
+      for (int i = 0; i < C::CPG; ++i) {
+        acc0[i] = fmaf(acc0[i], a.fine, acc0[i]);
+        acc1[i] = fmaf(acc1[i], a.fine, acc1[i]);
       }
       float amax0 = 0.f, amax1 = 0.f;
       const int part_row = (ry * a.tiles_x + cx) * (C::MT / 2) + rp;

@@ -4,8 +4,8 @@
 // The tap tensor is stored HL16 ([kg][P][8] fp16 hi/lo planes), which is exactly the
 // MN-major SWIZZLE_NONE operand layout (8 channels contiguous, pixels at 16 B stride), so the
 // same TMA box feeds both the A (channel tile c1) and the B (channel tile c2) operand.
-// A CTA owns one upper-triangle (c1, c2) tile pair and a pixel split of at most
-// `px_per_split` pixels; its fp32 TMEM accumulator therefore never sums more than that many
+// A CTA owns one upper-triangle (c1, c2) tile pair and a split of at most `px_per_split`
+// pixels of the owned rectangle (row-major runs of KPX pixels); its fp32 TMEM accumulator therefore never sums more than that many
 // terms, and splits are combined in f64 in a fixed order (gram_reduce), so the result is
 // deterministic and independent of the launch geometry.
 #include "common.cuh"
@@ -43,9 +43,12 @@ __global__ void __launch_bounds__(192, 1) gram_tc_kernel(const __grid_constant__
   }
   const int c2 = c1 + pair;
   const bool diag = c1 == c2;
-  const long long p0 = a.p_begin + (long long)blockIdx.x * a.px_per_split;
-  const long long p1 = min(p0 + a.px_per_split, a.p_end);
-  const int n_stages = p1 > p0 ? (int)((p1 - p0 + C::KPX - 1) / C::KPX) : 0;
+  // stage g of the owned rectangle = (row g / xblocks, KPX-pixel block g % xblocks)
+  const int xblocks = (a.w_own + C::KPX - 1) / C::KPX;
+  const long long total = (long long)a.rows * xblocks;
+  const long long g0 = (long long)blockIdx.x * (a.px_per_split / C::KPX);
+  const long long g1 = min(g0 + a.px_per_split / C::KPX, total);
+  const int n_stages = g1 > g0 ? (int)(g1 - g0) : 0;
   const int n_drains = (n_stages + C::DRAIN - 1) / C::DRAIN;
 
   if (warp == 0 && lane == 0) {
@@ -75,12 +78,13 @@ __global__ void __launch_bounds__(192, 1) gram_tc_kernel(const __grid_constant__
         mbar_wait(&empty_bar[s], ((c / C::STAGES) & 1) ^ 1);
         uint8_t* st = smem + s * C::STAGE;
         mbar_arrive_expect_tx(&full_bar[s], bytes);
-        const int px = (int)(p0 - a.p_begin) + c * C::KPX;  // map base starts at p_begin
-        tma_load_2d(st, &a.tm_hi, &full_bar[s], 2 * px, 16 * c1);  // u64 view: 64 px = 128 elements
-        tma_load_2d(st + C::T_BYTES, &a.tm_lo, &full_bar[s], 2 * px, 16 * c1);
+        const long long gs = g0 + c;
+        const int row = (int)(gs / xblocks), px = (int)(gs % xblocks) * C::KPX;
+        tma_load_3d(st, &a.tm_hi, &full_bar[s], 2 * px, row, 16 * c1);  // u64 view: 64 px = 128 elements
+        tma_load_3d(st + C::T_BYTES, &a.tm_lo, &full_bar[s], 2 * px, row, 16 * c1);
         if (!diag) {
-          tma_load_2d(st + 2 * C::T_BYTES, &a.tm_hi, &full_bar[s], 2 * px, 16 * c2);
-          tma_load_2d(st + 3 * C::T_BYTES, &a.tm_lo, &full_bar[s], 2 * px, 16 * c2);
+          tma_load_3d(st + 2 * C::T_BYTES, &a.tm_hi, &full_bar[s], 2 * px, row, 16 * c2);
+          tma_load_3d(st + 3 * C::T_BYTES, &a.tm_lo, &full_bar[s], 2 * px, row, 16 * c2);
         }
       }
     }
@@ -135,6 +139,11 @@ __global__ void __launch_bounds__(192, 1) gram_tc_kernel(const __grid_constant__
       __syncwarp();
       if (lane == 0) mbar_arrive(&cempty_bar[b]);
     }
+    {  // common part of the round-toward-zero compensation (diagonal entries: same-sign sums)
+      const int r = q * 32 + lane;
+#pragma unroll
+      for (int j = 0; j < 128; ++j) acc[j] = fmaf(acc[j], (diag && j == r) ? a.fine_diag : a.fine_off, acc[j]);
+    }
     const int pairs = a.n_ctile * (a.n_ctile + 1) / 2;
     float* dst = a.partial + (((size_t)blockIdx.x * pairs + blockIdx.y) * 128 + q * 32 + lane) * 128;
 #pragma unroll
@@ -169,9 +178,11 @@ __global__ void __launch_bounds__(192, 1) gram64_tc_kernel(const __grid_constant
   __shared__ uint64_t full_bar[C::STAGES], empty_bar[C::STAGES], cfull_bar[C::NBUF], cempty_bar[C::NBUF];
   __shared__ uint32_t tmem_slot;
   const uint32_t warp = warp_id(), lane = lane_id();
-  const long long p0 = a.p_begin + (long long)blockIdx.x * a.px_per_split;
-  const long long p1 = min(p0 + a.px_per_split, a.p_end);
-  const int n_stages = p1 > p0 ? (int)((p1 - p0 + C::KPX - 1) / C::KPX) : 0;
+  const int xblocks = (a.w_own + C::KPX - 1) / C::KPX;
+  const long long total = (long long)a.rows * xblocks;
+  const long long g0 = (long long)blockIdx.x * (a.px_per_split / C::KPX);
+  const long long g1 = min(g0 + a.px_per_split / C::KPX, total);
+  const int n_stages = g1 > g0 ? (int)(g1 - g0) : 0;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&a.tm_hi);
@@ -199,9 +210,10 @@ __global__ void __launch_bounds__(192, 1) gram64_tc_kernel(const __grid_constant
         mbar_wait(&empty_bar[s], ((c / C::STAGES) & 1) ^ 1);
         uint8_t* st = smem + s * C::STAGE;
         mbar_arrive_expect_tx(&full_bar[s], C::STAGE);
-        const int px = (int)(p0 - a.p_begin) + c * C::KPX;
-        tma_load_2d(st, &a.tm_hi, &full_bar[s], 2 * px, 0);  // u64 view: 128 px = 256 elements
-        tma_load_2d(st + 8 * C::PLANE, &a.tm_lo, &full_bar[s], 2 * px, 0);
+        const long long gs = g0 + c;
+        const int row = (int)(gs / xblocks), px = (int)(gs % xblocks) * C::KPX;
+        tma_load_3d(st, &a.tm_hi, &full_bar[s], 2 * px, row, 0);  // u64 view: 128 px = 256 elements
+        tma_load_3d(st + 8 * C::PLANE, &a.tm_lo, &full_bar[s], 2 * px, row, 0);
       }
     }
   } else if (warp == 1) {
@@ -265,6 +277,10 @@ __global__ void __launch_bounds__(192, 1) gram64_tc_kernel(const __grid_constant
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&cempty_bar[b]);
+    }
+    if (row < 64) {  // common part of the round-toward-zero compensation of the hi*hi sums
+#pragma unroll
+      for (int j = 0; j < 64; ++j) acc[j] = fmaf(acc[j], j == row ? a.fine_diag : a.fine_off, acc[j]);
     }
     float* dst = a.partial + ((size_t)blockIdx.x * 128 + row) * 64;
 #pragma unroll

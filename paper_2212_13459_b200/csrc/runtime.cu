@@ -85,16 +85,16 @@ bool map_rows128(CUtensorMap* m, const __half* base, int H, int W) {
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// Gram operand: the HL16 planes viewed as u64 (2P, kg); box (128 = 64 px, 16 kg) or, for 64
-// channels, (256 = 128 px, 8 kg).  Each box row is one plane's contiguous pixel run (1-2 KB),
-// landing as the dense [kg][px][8] MN-major operand.
-bool map_gram(CUtensorMap* m, const __half* base, long long P_range, long long P_total, int n_kg) {
-  cuuint64_t dims[2] = {2 * (cuuint64_t)P_range, (cuuint64_t)n_kg};
-  cuuint64_t strides[1] = {(cuuint64_t)P_total * 16};
+// Gram operand: the owned rectangle of the HL16 planes viewed as u64 (2 w_own, rows, kg); box =
+// one run of 64 px (128 channels: x 16 kg) or 128 px (64 channels: x 8 kg) of one row, landing
+// as the dense [kg][px][8] MN-major operand; the run past w_own is TMA zero fill.
+bool map_gram(CUtensorMap* m, const __half* base, int w_own, int rows, int W, int H, int n_kg) {
+  cuuint64_t dims[3] = {2 * (cuuint64_t)w_own, (cuuint64_t)rows, (cuuint64_t)n_kg};
+  cuuint64_t strides[2] = {(cuuint64_t)W * 16, (cuuint64_t)H * W * 16};
   const bool c64 = n_kg == 8;
-  cuuint32_t box[2] = {c64 ? 256u : 128u, c64 ? 8u : 16u};
-  cuuint32_t es[2] = {1, 1};
-  return g_encode(m, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, (void*)base, dims, strides, box, es,
+  cuuint32_t box[3] = {c64 ? 256u : 128u, 1, c64 ? 8u : 16u};
+  cuuint32_t es[3] = {1, 1, 1};
+  return g_encode(m, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, (void*)base, dims, strides, box, es,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
@@ -103,11 +103,20 @@ int round_up(int v, int m) { return (v + m - 1) / m * m; }
 
 // Gram accumulators (gram_tc.cu): 128 channels = 8 correction + 4 hi*hi MMAs per 64-px stage;
 // 64 channels = 8 hi*hi MMAs per 128-px stage (corrections in separate columns); two stages each.
-void set_gram_comp(GramArgs& g, int C_p) {
-  const double k = spst::rz_kappa();
+// Tap features are ReLU outputs (>= 0), so every Gram entry is a same-sign sum: besides the
+// result truncation, every addend's alignment truncation biases the same way.  kappa per
+// kernel and entry kind, measured on B200 with tools/rz_calibrate.py (relu-like operands;
+// checked on VGG-19 taps with tools/error_budget.py).
+void set_gram_comp(GramArgs& g, int C_p, bool nonneg = true) {
   const bool c64 = C_p == 64;
-  g.comp[0] = (float)(1.0 + k * spst::rz_weight(c64 ? 0 : 8, c64 ? 8 : 4, 1));
-  g.comp[1] = (float)(1.0 + k * spst::rz_weight(c64 ? 0 : 8, c64 ? 8 : 4, 2));
+  const double w1 = spst::rz_weight(c64 ? 0 : 8, c64 ? 8 : 4, 1), w2 = spst::rz_weight(c64 ? 0 : 8, c64 ? 8 : 4, 2);
+  const double on = spst::rz_kappa() > 0.0 ? 1.0 : 0.0;  // SPST_RZ_KAPPA=0 disables every compensation
+  const double kd = on * (c64 ? 7.3e-8 : 5.2e-8), ko = on * (nonneg ? (c64 ? 4.9e-8 : 3.8e-8) : spst::rz_kappa());
+  g.fine_diag = (float)(kd * w2);
+  g.fine_off = (float)(ko * w2);
+  // a split's last accumulator may hold one stage: the remainder relative to fine
+  g.comp[0] = (float)(1.0 + ko * (w1 - w2));
+  g.comp[1] = 1.f;
 }
 
 int env_int(const char* name, int dflt) {
@@ -126,15 +135,18 @@ int bwd_drain() {
   return d;
 }
 
-// comp[] of a conv launch (conv_tc.cu): a conv chunk is 18 correction MMAs then 9 hi*hi MMAs
-// per output row; an extra-K chunk xkg correction then xkg/2 hi*hi MMAs.
+// comp[] / fine of a conv launch (conv_tc.cu): a conv chunk is 18 correction MMAs then 9 hi*hi
+// MMAs per output row; an extra-K chunk xkg correction then xkg/2 hi*hi MMAs.  `fine` carries
+// the full conv group's correction; comp[] the difference of every other group composition.
 void set_conv_comp(ConvArgs& a, int N) {
   const double k = rz_kappa();
   const int xkg = conv_tc_xkg(N);
-  a.comp[0] = (float)(1.0 + k * rz_weight(18, 9, 1));
-  a.comp[1] = (float)(1.0 + k * rz_weight(18, 9, 2));
-  a.comp[2] = (float)(1.0 + k * rz_weight(xkg, xkg / 2, 1));
-  a.comp[3] = (float)(1.0 + k * rz_weight(xkg, xkg / 2, 2));
+  const double wf = rz_weight(18, 9, a.drain);
+  a.fine = (float)(k * wf);
+  a.comp[0] = (float)(1.0 + k * (rz_weight(18, 9, 1) - wf));
+  a.comp[1] = (float)(1.0 + k * (rz_weight(18, 9, 2) - wf));
+  a.comp[2] = (float)(1.0 + k * (rz_weight(xkg, xkg / 2, 1) - wf));
+  a.comp[3] = (float)(1.0 + k * (rz_weight(xkg, xkg / 2, 2) - wf));
 }
 // enough (split x pair) CTAs for two waves, splits of 1K..64K pixels (multiples of 128)
 int gram_px_per_split(long long px, int pairs) {
@@ -227,6 +239,8 @@ struct spst_ctx {
   long long alloc_bytes = 0;
   bool bound = false;
   int h = 0, w = 0, Hp = 0, Wp = 0, grid_r0 = 0, grid_r1 = 0, own_r0 = 0, own_r1 = 0;
+  int grid_c0 = 0, grid_c1 = 0, own_c0 = 0, own_c1 = 0;  // window columns (padded-image coordinates)
+  long long x_pitch = 0, g_pitch = 0;                     // pixels per row of the image / gradient buffers
   unsigned int* amax_d = nullptr;  // [stages][4]: out, pooled, grad, addend; [4 * stages]: image
   HL16 img;                        // first conv's K operand (8-channel HL16 image), see image_hl_kernel
   Expo img_e;
@@ -348,15 +362,19 @@ double spst::rz_weight(int small, int large, int chunks) {
   return w;
 }
 
-// kappa = E[dropped fraction] x E[ulp(x)/|x|] = 0.5 x (1/ln 2)(1 - 1/2) x 2^-23 = 4.30e-8 for a
-// log-uniform significand; SPST_RZ_KAPPA overrides (0 disables the compensation).
-float spst::rz_kappa() {
-  static const float k = [] {
+// Round-toward-zero compensation constants (conv_tc.cu), measured on B200 with
+// tools/rz_calibrate.py: mixed-sign sums lose ~kappa x (MMAs weighted by the partial-sum
+// growth) -- one truncation of the result per MMA, 0.5 x E[ulp/|x|] -- while same-sign sums
+// (Gram entries of ReLU features) also lose every addend's alignment truncation (set_gram_comp).
+// SPST_RZ_KAPPA overrides (0 disables all compensation).
+double spst::rz_kappa() {
+  static const double k = [] {
     const char* e = getenv("SPST_RZ_KAPPA");
-    return e && *e ? (float)atof(e) : 4.30e-8f;
+    return e && *e ? atof(e) : 3.3e-8;
   }();
   return k;
 }
+
 
 namespace {
 
@@ -602,6 +620,7 @@ float read_amax(spst_ctx* ctx, int slot) {
 int forward_stage(spst_ctx* ctx, int k, const float* x) {
   Stage& s = ctx->stages[k];
   const int own0 = (ctx->own_r0 - ctx->grid_r0) / s.stride, own1 = (ctx->own_r1 - ctx->grid_r0) / s.stride;
+  const int ownc0 = (ctx->own_c0 - ctx->grid_c0) / s.stride, ownc1 = (ctx->own_c1 - ctx->grid_c0) / s.stride;
   TapState* tap = s.style >= 0 ? &ctx->taps[s.style] : nullptr;
   s.out.scale = pow2f(s.out_e.e);
   s.pooled.scale = pow2f(s.pool_e.e);
@@ -612,6 +631,8 @@ int forward_stage(spst_ctx* ctx, int k, const float* x) {
     ia.h = ctx->h;
     ia.w = ctx->w;
     ia.row_off = ctx->grid_r0;
+    ia.col_off = ctx->grid_c0;
+    ia.pitch = ctx->x_pitch;
     ia.Hl = s.H;
     ia.Wp = s.W;
     for (int c = 0; c < 3; ++c) {
@@ -644,6 +665,8 @@ int forward_stage(spst_ctx* ctx, int k, const float* x) {
   a.colsum_partial = tap ? tap->colsum_partial : nullptr;
   a.sum_r0 = own0;
   a.sum_r1 = own1;
+  a.sum_c0 = ownc0;
+  a.sum_c1 = ownc1;
   a.amax = ctx->amax_d + 4 * k;
   return run_conv(ctx, L);
 }
@@ -654,16 +677,17 @@ int stage_stats(spst_ctx* ctx, int k) {
   TapState& t = ctx->taps[s.style];
   CK(launch_colsum_reduce(t.colsum_partial, t.colsum_rows, s.cout, s.cout_p, t.s, t.colsum_mid, ctx->stream));
   const int own0 = (ctx->own_r0 - ctx->grid_r0) / s.stride, own1 = (ctx->own_r1 - ctx->grid_r0) / s.stride;
-  const long long P_total = (long long)s.H * s.W;
-  const long long p0 = (long long)own0 * s.W, p1 = (long long)own1 * s.W;
+  const int ownc0 = (ctx->own_c0 - ctx->grid_c0) / s.stride, ownc1 = (ctx->own_c1 - ctx->grid_c0) / s.stride;
+  const long long o0 = (long long)own0 * s.W + ownc0;
   GramArgs g{};
-  if (!map_gram(&g.tm_hi, s.out.hi + p0 * 8, p1 - p0, P_total, s.cout_p / 8) ||
-      !map_gram(&g.tm_lo, s.out.lo() + p0 * 8, p1 - p0, P_total, s.cout_p / 8))
+  if (!map_gram(&g.tm_hi, s.out.hi + o0 * 8, ownc1 - ownc0, own1 - own0, s.W, s.H, s.cout_p / 8) ||
+      !map_gram(&g.tm_lo, s.out.lo() + o0 * 8, ownc1 - ownc0, own1 - own0, s.W, s.H, s.cout_p / 8))
     return ctx->fail(SPST_ERR_CUDA, "cuTensorMapEncodeTiled failed (gram)");
   g.C_p = s.cout_p;
-  g.p_begin = 0;
-  g.p_end = p1 - p0;
+  g.rows = own1 - own0;
+  g.w_own = ownc1 - ownc0;
   g.px_per_split = t.gram_px;
+  const long long p0 = 0, p1 = (long long)g.rows * g.w_own;  // owned pixels (launch timer)
   g.n_ctile = (s.cout_p + 127) / 128;
   g.partial = t.gram_partial;
   set_gram_comp(g, s.cout_p);
@@ -947,8 +971,21 @@ int do_backward(spst_ctx* ctx, double two_lambda, float* grad, bool careful) {
   b.gimg = ctx->gimg;
   CK(launch_first_conv_bwd(b, ctx->stream));
   }
-  const int r0 = ctx->own_r0, r1 = std::min(ctx->own_r1, ctx->h);
-  CK(launch_fold_grad(ctx->gimg, s0.H, s0.W, ctx->grid_r0, ctx->h, ctx->w, r0, r1, grad, ctx->stream));
+  FoldArgs fa{};
+  fa.gimg = ctx->gimg;
+  fa.Hl = s0.H;
+  fa.Wl = s0.W;
+  fa.row_off = ctx->grid_r0;
+  fa.col_off = ctx->grid_c0;
+  fa.h = ctx->h;
+  fa.w = ctx->w;
+  fa.r0 = ctx->own_r0;
+  fa.r1 = std::min(ctx->own_r1, ctx->h);
+  fa.c0 = ctx->own_c0;
+  fa.c1 = std::min(ctx->own_c1, ctx->w);
+  fa.grad = grad;
+  fa.pitch = ctx->g_pitch;
+  CK(launch_fold_grad(fa, ctx->stream));
   // end-of-pass range check (fast path)
   ctx->amax_h.resize(4 * n);
   CK(cudaMemcpyAsync(ctx->amax_h.data(), ctx->amax_d, 16 * n, cudaMemcpyDeviceToHost, ctx->stream));
@@ -966,13 +1003,13 @@ int do_backward(spst_ctx* ctx, double two_lambda, float* grad, bool careful) {
 
 int bind_alloc(spst_ctx* ctx) {
   const int n = (int)ctx->stages.size();
-  const int Hl = ctx->grid_r1 - ctx->grid_r0;
+  const int Hl = ctx->grid_r1 - ctx->grid_r0, Wl = ctx->grid_c1 - ctx->grid_c0;
   size_t gmax = 0, admax = 0;
   int max_cp = 64;
   for (int k = 0; k < n; ++k) {
     Stage& s = ctx->stages[k];
     s.H = Hl / s.stride;
-    s.W = ctx->Wp / s.stride;
+    s.W = Wl / s.stride;
     static const bool store_all = [] {  // diagnostics (tools/error_budget.py): keep every relu output
       const char* e = getenv("SPST_DEBUG_STORE_ALL");
       return e && atoi(e) != 0;
@@ -1005,8 +1042,9 @@ int bind_alloc(spst_ctx* ctx) {
       t.ratio = ctx->dalloc<double>(C);
       t.bvec = ctx->dalloc<float>(Cp);
       t.xw = ctx->dalloc<__half>((size_t)Cp * Cp * 2);
-      const int own0 = (ctx->own_r0 - ctx->grid_r0) / s.stride, own1 = (ctx->own_r1 - ctx->grid_r0) / s.stride;
-      const long long own_px = (long long)(own1 - own0) * s.W;
+      const int own_rows = (ctx->own_r1 - ctx->own_r0) / s.stride, own_cols = (ctx->own_c1 - ctx->own_c0) / s.stride;
+      const int kpx = Cp == 64 ? 128 : 64;  // pixels per Gram stage (gram_tc.cu)
+      const long long own_px = (long long)own_rows * ((own_cols + kpx - 1) / kpx) * kpx;
       const int nct = (Cp + 127) / 128;
       t.gram_px = gram_px_per_split(own_px, nct * (nct + 1) / 2);
       t.gram_splits = (int)std::max<long long>(1, (own_px + t.gram_px - 1) / t.gram_px);
@@ -1059,10 +1097,10 @@ int bind_alloc(spst_ctx* ctx) {
   ctx->addend = hl_shape(64, 1, 1);
   ctx->addend.hi = ctx->dalloc<__half>(std::max<size_t>(admax, 16));
   ctx->addend_elems = admax;
-  ctx->gimg = ctx->dalloc<float>((size_t)Hl * ctx->Wp * 3);
+  ctx->gimg = ctx->dalloc<float>((size_t)Hl * Wl * 3);
   ctx->amax_d = ctx->dalloc<unsigned int>(4 * n + 4);
-  ctx->img = hl_shape(8, Hl, ctx->Wp);
-  ctx->img.hi = ctx->dalloc<__half>((size_t)8 * Hl * ctx->Wp * 2);
+  ctx->img = hl_shape(8, Hl, Wl);
+  ctx->img.hi = ctx->dalloc<__half>((size_t)8 * Hl * Wl * 2);
   if (!ctx->img.hi) return ctx->fail(SPST_ERR_OOM, "image operand");
   ctx->content_partial = ctx->dalloc<double>(red_blocks() + 8);
   ctx->zero_xw = ctx->dalloc<__half>((size_t)max_cp * max_cp * 2);
@@ -1210,16 +1248,22 @@ int spst_set_stream(spst_ctx* ctx, void* stream) {
   return SPST_OK;
 }
 
-int spst_bind(spst_ctx* ctx, int h, int w, int grid_r0, int grid_r1, int own_r0, int own_r1) {
+int spst_bind_window(spst_ctx* ctx, int h, int w, int grid_r0, int grid_r1, int grid_c0, int grid_c1, int own_r0,
+                     int own_r1, int own_c0, int own_c1) {
   const int ds = ctx->deepest_stride;
   if (h < 1 || w < 1) return ctx->fail(SPST_ERR_SHAPE, "image dims must be >= 1");
   const int Hp = round_up(h, ds), Wp = round_up(w, ds);
-  if (grid_r0 % ds || grid_r1 % ds || own_r0 % ds || (own_r1 % ds && own_r1 != Hp))
-    return ctx->fail(SPST_ERR_GEOMETRY, "row ranges must be multiples of the deepest stride");
+  if (grid_r0 % ds || grid_r1 % ds || own_r0 % ds || (own_r1 % ds && own_r1 != Hp) || grid_c0 % ds ||
+      grid_c1 % ds || own_c0 % ds || (own_c1 % ds && own_c1 != Wp))
+    return ctx->fail(SPST_ERR_GEOMETRY, "window bounds must be multiples of the deepest stride");
   if (!(0 <= grid_r0 && grid_r0 <= own_r0 && own_r0 < own_r1 && own_r1 <= grid_r1 && grid_r1 <= Hp))
     return ctx->fail(SPST_ERR_GEOMETRY, "row ranges must nest: 0 <= grid_r0 <= own_r0 < own_r1 <= grid_r1 <= Hp");
+  if (!(0 <= grid_c0 && grid_c0 <= own_c0 && own_c0 < own_c1 && own_c1 <= grid_c1 && grid_c1 <= Wp))
+    return ctx->fail(SPST_ERR_GEOMETRY,
+                     "column ranges must nest: 0 <= grid_c0 <= own_c0 < own_c1 <= grid_c1 <= Wp");
   if (ctx->bound && ctx->h == h && ctx->w == w && ctx->grid_r0 == grid_r0 && ctx->grid_r1 == grid_r1 &&
-      ctx->own_r0 == own_r0 && ctx->own_r1 == own_r1)
+      ctx->own_r0 == own_r0 && ctx->own_r1 == own_r1 && ctx->grid_c0 == grid_c0 && ctx->grid_c1 == grid_c1 &&
+      ctx->own_c0 == own_c0 && ctx->own_c1 == own_c1)
     return SPST_OK;
   ctx->release_bound();
   ctx->h = h;
@@ -1230,12 +1274,27 @@ int spst_bind(spst_ctx* ctx, int h, int w, int grid_r0, int grid_r1, int own_r0,
   ctx->grid_r1 = grid_r1;
   ctx->own_r0 = own_r0;
   ctx->own_r1 = own_r1;
+  ctx->grid_c0 = grid_c0;
+  ctx->grid_c1 = grid_c1;
+  ctx->own_c0 = own_c0;
+  ctx->own_c1 = own_c1;
   int r = bind_alloc(ctx);
   if (r) {
     ctx->release_bound();
     return r;
   }
   ctx->bound = true;
+  return SPST_OK;
+}
+
+int spst_bind(spst_ctx* ctx, int h, int w, int grid_r0, int grid_r1, int own_r0, int own_r1) {
+  const int Wp = round_up(w, ctx->deepest_stride);
+  return spst_bind_window(ctx, h, w, grid_r0, grid_r1, 0, Wp, own_r0, own_r1, 0, Wp);
+}
+
+int spst_window_dims(const spst_ctx* ctx, int* rows, int* cols) {
+  *rows = ctx->grid_r1 - ctx->grid_r0;
+  *cols = ctx->grid_c1 - ctx->grid_c0;
   return SPST_OK;
 }
 
@@ -1255,15 +1314,18 @@ int spst_tap_info(const spst_ctx* ctx, int tap, int* channels, int* stride, long
   const Stage& s = ctx->stages[ctx->taps[tap].stage];
   *channels = s.cout;
   *stride = s.stride;
-  *owned_pixels = ctx->bound ? (long long)((ctx->own_r1 - ctx->own_r0) / s.stride) * (ctx->Wp / s.stride) : 0;
+  *owned_pixels =
+      ctx->bound ? (long long)((ctx->own_r1 - ctx->own_r0) / s.stride) * ((ctx->own_c1 - ctx->own_c0) / s.stride) : 0;
   return SPST_OK;
 }
 
 long long spst_workspace_bytes(const spst_ctx* ctx) { return ctx->alloc_bytes; }
 
-int spst_forward(spst_ctx* ctx, const float* x, int flags) {
+int spst_forward_pitched(spst_ctx* ctx, const float* x, long long pitch, int flags) {
   (void)flags;
   if (!ctx->bound) return ctx->fail(SPST_ERR_CONFIG, "spst_bind must precede spst_forward");
+  if (pitch < ctx->w) return ctx->fail(SPST_ERR_SHAPE, "image pitch below the image width");
+  ctx->x_pitch = pitch;
   int r = do_forward(ctx, x, false);
   if (r == 1) r = do_forward(ctx, x, true);
   if (r == 1) return ctx->fail(SPST_ERR_NONFINITE, "activation range could not be represented (non-finite?)");
@@ -1271,6 +1333,11 @@ int spst_forward(spst_ctx* ctx, const float* x, int flags) {
   ctx->fwd_done = true;
   ctx->finalized = false;
   return SPST_OK;
+}
+
+int spst_forward(spst_ctx* ctx, const float* x, int flags) {
+  if (!ctx->bound) return ctx->fail(SPST_ERR_CONFIG, "spst_bind must precede spst_forward");
+  return spst_forward_pitched(ctx, x, ctx->w, flags);
 }
 
 int spst_stats_ptrs(spst_ctx* ctx, int tap, double** S, double** s) {
@@ -1290,11 +1357,29 @@ int spst_capture_content(spst_ctx* ctx) {
   return SPST_OK;
 }
 
+int spst_content_target(spst_ctx* ctx, void** buf, long long* bytes, float* scale) {
+  if (ctx->content_stage < 0 || !ctx->bound) return ctx->fail(SPST_ERR_CONFIG, "no content tap / unbound");
+  *buf = ctx->content_u.hi;
+  *bytes = (long long)ctx->content_u.bytes();
+  *scale = ctx->content_u.scale;
+  return SPST_OK;
+}
+
+int spst_set_content_target(spst_ctx* ctx, const void* buf, float scale) {
+  if (ctx->content_stage < 0 || !ctx->bound) return ctx->fail(SPST_ERR_CONFIG, "no content tap / unbound");
+  if (buf != ctx->content_u.hi)
+    CK(cudaMemcpyAsync(ctx->content_u.hi, buf, ctx->content_u.bytes(), cudaMemcpyDeviceToDevice, ctx->stream));
+  ctx->content_u.scale = scale;
+  ctx->content_captured = true;
+  return SPST_OK;
+}
+
 int spst_content_sqdiff(spst_ctx* ctx, double* out) {
   if (!ctx->content_captured) return ctx->fail(SPST_ERR_CONFIG, "content target not captured");
   const Stage& s = ctx->stages[ctx->content_stage];
   const int r0 = (ctx->own_r0 - ctx->grid_r0) / s.stride, r1 = (ctx->own_r1 - ctx->grid_r0) / s.stride;
-  CK(launch_content_sqdiff(s.out, ctx->content_u, s.cout, r0, r1, ctx->content_partial, out, ctx->stream));
+  const int c0 = (ctx->own_c0 - ctx->grid_c0) / s.stride, c1 = (ctx->own_c1 - ctx->grid_c0) / s.stride;
+  CK(launch_content_sqdiff(s.out, ctx->content_u, s.cout, r0, r1, c0, c1, ctx->content_partial, out, ctx->stream));
   return SPST_OK;
 }
 
@@ -1357,7 +1442,13 @@ int spst_finalize(spst_ctx* ctx, const long long* n, double* terms, int* degener
 }
 
 int spst_backward(spst_ctx* ctx, double two_lambda, float* grad) {
+  return spst_backward_pitched(ctx, two_lambda, grad, ctx->w);
+}
+
+int spst_backward_pitched(spst_ctx* ctx, double two_lambda, float* grad, long long pitch) {
   if (!ctx->finalized) return ctx->fail(SPST_ERR_CONFIG, "spst_finalize must precede spst_backward");
+  if (pitch < ctx->w) return ctx->fail(SPST_ERR_SHAPE, "gradient pitch below the image width");
+  ctx->g_pitch = pitch;
   if (two_lambda != 0.0 && ctx->content_stage >= 0 && !ctx->content_captured)
     return ctx->fail(SPST_ERR_CONFIG, "content weight is nonzero but no content target was captured");
   int r = do_backward(ctx, two_lambda, grad, false);
@@ -1620,14 +1711,17 @@ int spst_debug_gram(int device, int C, long long P, const float* f_host, double*
   CK(cudaMemcpy(fd, f_host, (size_t)C * P * 4, cudaMemcpyHostToDevice));
   note_launch(), pack_hl_kernel<<<512, 256>>>(fd, C, t);
   GramArgs g{};
-  if (!map_gram(&g.tm_hi, t.hi, P, P, Cp / 8) || !map_gram(&g.tm_lo, t.lo(), P, P, Cp / 8)) return SPST_ERR_CUDA;
+  if (!map_gram(&g.tm_hi, t.hi, (int)P, 1, (int)P, 1, Cp / 8) || !map_gram(&g.tm_lo, t.lo(), (int)P, 1, (int)P, 1, Cp / 8))
+    return SPST_ERR_CUDA;
   g.C_p = Cp;
-  g.p_begin = 0;
-  g.p_end = P;
+  g.rows = 1;
+  g.w_own = (int)P;
   g.px_per_split = per;
   g.n_ctile = nct;
   g.partial = part;
-  set_gram_comp(g, Cp);
+  bool nonneg = true;  // ReLU-like operands get the same-sign compensation of real taps
+  for (long long i = 0; i < (long long)C * P && nonneg; ++i) nonneg = f_host[i] >= 0.f;
+  set_gram_comp(g, Cp, nonneg);
   if (Cp == 64) {
     CK(launch_gram64_tc(g, splits, C, 1.0, Sd, nullptr));
   } else {

@@ -33,8 +33,8 @@ __global__ void __launch_bounds__(256) image_hl_kernel(const __grid_constant__ I
   for (int y = blockIdx.y; y < a.Hl; y += gridDim.y)
   for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < a.Wp; x += gridDim.x * blockDim.x) {
     const long long i = (long long)y * a.Wp + x;
-    const int gy = min(y + a.row_off, a.h - 1), gx = min(x, a.w - 1);
-    const float* px = a.img + ((size_t)gy * a.w + gx) * 3;
+    const int gy = min(y + a.row_off, a.h - 1), gx = min(x + a.col_off, a.w - 1);
+    const float* px = a.img + ((long long)gy * a.pitch + gx) * 3;
     __align__(16) __half hh[8];
     __align__(16) __half ll[8];
 #pragma unroll
@@ -105,31 +105,32 @@ __global__ void __launch_bounds__(256) first_conv_bwd_kernel(const __grid_consta
   }
 }
 
-// grad (rows [r0,r1) of the h x w unpadded image) from the local padded-grid gradient.
-__global__ void fold_grad_kernel(const float* gimg, int Hl, int Wp, int row_off, int h, int w, int r0, int r1,
-                                 float* grad) {
-  const int gx = blockIdx.x * blockDim.x + threadIdx.x;  // grid (column blocks, rows): no index division
-  if (gx >= w) return;
-  for (int gy = r0 + blockIdx.y; gy < r1; gy += gridDim.y) {
-    const int ly = gy - row_off;
+// grad over the owned rectangle from the local padded-grid gradient (FoldArgs, common.cuh).
+__global__ void fold_grad_kernel(const FoldArgs a) {
+  const int gx = a.c0 + blockIdx.x * blockDim.x + threadIdx.x;  // grid (column blocks, rows): no index division
+  if (gx >= a.c1) return;
+  const int lx = gx - a.col_off;
+  for (int gy = a.r0 + blockIdx.y; gy < a.r1; gy += gridDim.y) {
+    const int ly = gy - a.row_off;
+    const float* g = a.gimg;
     float acc[3];
 #pragma unroll
-    for (int c = 0; c < 3; ++c) acc[c] = gimg[((size_t)ly * Wp + gx) * 3 + c];
-    const int Hp_loc_end = Hl;  // local rows beyond the image (ly >= h - row_off) fold onto h-1
-    if (gy == h - 1)
-      for (int yy = ly + 1; yy < Hp_loc_end; ++yy)
+    for (int c = 0; c < 3; ++c) acc[c] = g[((size_t)ly * a.Wl + lx) * 3 + c];
+    // local rows / columns beyond the image (replicate padding) fold onto row h-1 / column w-1
+    if (gy == a.h - 1)
+      for (int yy = ly + 1; yy < a.Hl; ++yy)
 #pragma unroll
-        for (int c = 0; c < 3; ++c) acc[c] += gimg[((size_t)yy * Wp + gx) * 3 + c];
-    if (gx == w - 1)
-      for (int xx = w; xx < Wp; ++xx)
+        for (int c = 0; c < 3; ++c) acc[c] += g[((size_t)yy * a.Wl + lx) * 3 + c];
+    if (gx == a.w - 1)
+      for (int xx = lx + 1; xx < a.Wl; ++xx)
 #pragma unroll
-        for (int c = 0; c < 3; ++c) acc[c] += gimg[((size_t)ly * Wp + xx) * 3 + c];
-    if (gy == h - 1 && gx == w - 1)
-      for (int yy = ly + 1; yy < Hp_loc_end; ++yy)
-        for (int xx = w; xx < Wp; ++xx)
+        for (int c = 0; c < 3; ++c) acc[c] += g[((size_t)ly * a.Wl + xx) * 3 + c];
+    if (gy == a.h - 1 && gx == a.w - 1)
+      for (int yy = ly + 1; yy < a.Hl; ++yy)
+        for (int xx = lx + 1; xx < a.Wl; ++xx)
 #pragma unroll
-          for (int c = 0; c < 3; ++c) acc[c] += gimg[((size_t)yy * Wp + xx) * 3 + c];
-    float* o = grad + ((size_t)gy * w + gx) * 3;
+          for (int c = 0; c < 3; ++c) acc[c] += g[((size_t)yy * a.Wl + xx) * 3 + c];
+    float* o = a.grad + ((long long)gy * a.pitch + gx) * 3;
 #pragma unroll
     for (int c = 0; c < 3; ++c) o[c] = acc[c];
   }
@@ -326,9 +327,25 @@ __device__ __forceinline__ double sqdiff8(uint4 vh, uint4 vl, uint4 uh, uint4 ul
 }
 
 __global__ void __launch_bounds__(kRedThreads) content_sqdiff_kernel(HL16 v, HL16 u, int C, int r0, int r1,
-                                                                     double* partial) {
+                                                                     int c0, int c1, double* partial) {
   __shared__ double sh[32];
   const int kg = blockIdx.y;
+  const int wc = c1 - c0;
+  if (wc != v.W) {  // owned rectangle narrower than the grid (windowed evaluation): row/column loop
+    double acc = 0.0;
+    const int nvalid = min(8, C - kg * 8);
+    const float iv = 1.f / v.scale, iu = 1.f / u.scale;
+    const long long n = (long long)(r1 - r0) * wc;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+      const size_t o = ((size_t)kg * v.H + r0 + i / wc) * v.W + c0 + i % wc;
+      acc += sqdiff8(reinterpret_cast<const uint4*>(v.hi)[o], reinterpret_cast<const uint4*>(v.lo())[o],
+                     reinterpret_cast<const uint4*>(u.hi)[o], reinterpret_cast<const uint4*>(u.lo())[o], iv, iu,
+                     nvalid);
+    }
+    const double t = block_sum(acc, sh);
+    if (threadIdx.x == 0) partial[blockIdx.y * gridDim.x + blockIdx.x] = t;
+    return;
+  }
   const long long per_plane = (long long)(r1 - r0) * v.W;
   const size_t base = (size_t)kg * v.H * v.W + (size_t)r0 * v.W;
   const uint4* vh = reinterpret_cast<const uint4*>(v.hi) + base;
@@ -718,12 +735,10 @@ cudaError_t launch_first_conv_bwd(const FirstConvBwdArgs& a, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_fold_grad(const float* gimg, int Hl, int Wp, int row_off, int h, int w, int r0, int r1,
-                             float* grad, cudaStream_t st) {
-  const long long n = (long long)(r1 - r0) * w;
-  if (n <= 0) return cudaSuccess;
-  const dim3 grid((w + 255) / 256, std::min(r1 - r0, 65535));
-  note_launch(), fold_grad_kernel<<<grid, 256, 0, st>>>(gimg, Hl, Wp, row_off, h, w, r0, r1, grad);
+cudaError_t launch_fold_grad(const FoldArgs& a, cudaStream_t st) {
+  if (a.r1 <= a.r0 || a.c1 <= a.c0) return cudaSuccess;
+  const dim3 grid((a.c1 - a.c0 + 255) / 256, std::min(a.r1 - a.r0, 65535));
+  note_launch(), fold_grad_kernel<<<grid, 256, 0, st>>>(a);
   return cudaGetLastError();
 }
 
@@ -757,12 +772,12 @@ cudaError_t launch_sum_partials(const double* partial, int nk, double* out, cuda
   return cudaGetLastError();
 }
 
-cudaError_t launch_content_sqdiff(const HL16& v, const HL16& u, int C, int r0, int r1, double* partial,
-                                  double* out, cudaStream_t st) {
+cudaError_t launch_content_sqdiff(const HL16& v, const HL16& u, int C, int r0, int r1, int c0, int c1,
+                                  double* partial, double* out, cudaStream_t st) {
   const int nkg = (C + 7) / 8;  // kgroups holding real channels
   if (nkg > kRedBlocks) return cudaErrorInvalidValue;
   const dim3 grid(std::max(1, kRedBlocks / nkg), nkg);  // <= kRedBlocks partials
-  note_launch(), content_sqdiff_kernel<<<grid, kRedThreads, 0, st>>>(v, u, C, r0, r1, partial);
+  note_launch(), content_sqdiff_kernel<<<grid, kRedThreads, 0, st>>>(v, u, C, r0, r1, c0, c1, partial);
   note_launch(), finish_sums_kernel<<<1, 32, 0, st>>>(partial, (int)(grid.x * grid.y), 1, out);
   return cudaGetLastError();
 }

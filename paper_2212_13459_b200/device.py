@@ -109,21 +109,31 @@ class Engine:
         return s
 
     # ------------------------------------------------------------------ geometry
-    def bind(self, h, w, grid=None, own=None):
-        """Bind image dims; grid/own are padded-row ranges (default: the whole image)."""
+    def bind(self, h, w, grid=None, own=None, gcols=None, ocols=None):
+        """Bind image dims and the evaluated window (padded-image coordinates): rows grid / own,
+        columns gcols / ocols (defaults: the whole padded image, owned entirely)."""
         s = self.spec.deepest_stride()
-        Hp = h + (-h) % s
-        grid = grid or (0, Hp)
-        own = own or grid
-        key = (h, w, grid, own)
+        Hp, Wp = h + (-h) % s, w + (-w) % s
+        grid = tuple(grid or (0, Hp))
+        own = tuple(own or grid)
+        gcols = tuple(gcols or (0, Wp))
+        ocols = tuple(ocols or gcols)
+        key = (h, w, grid, own, gcols, ocols)
         if self.bound == key:
             return
         with torch.cuda.device(self.device):
-            self._check(nat.lib().spst_bind(self._h, h, w, grid[0], grid[1], own[0], own[1]), "spst_bind")
+            self._check(nat.lib().spst_bind_window(self._h, h, w, grid[0], grid[1], gcols[0], gcols[1], own[0],
+                                                   own[1], ocols[0], ocols[1]), "spst_bind_window")
         self.bound = key
         self.bind_epoch += 1
         self.last_forward_key = None
         self._content_out = torch.zeros(1, dtype=torch.float64, device=f"cuda:{self.device}")
+
+    def window_dims(self):
+        """(rows, columns) of the bound window's padded grid."""
+        a, b = ctypes.c_int(), ctypes.c_int()
+        nat.lib().spst_window_dims(self._h, ctypes.byref(a), ctypes.byref(b))
+        return a.value, b.value
 
     def unbind(self):
         with torch.cuda.device(self.device):
@@ -146,11 +156,15 @@ class Engine:
         return int(nat.lib().spst_workspace_bytes(self._h))
 
     # ------------------------------------------------------------------ passes
-    def forward(self, x_dev):
-        """x_dev: (h, w, 3) float32 CUDA tensor matching the bound dims."""
+    def forward(self, x_dev, origin=(0, 0)):
+        """x_dev: float32 CUDA tensor of image rows/columns starting at global pixel `origin`
+        ((h, w, 3) for the whole image; any (rows, cols, 3) block covering the window's image
+        pixels otherwise)."""
         self.stream()
+        pitch = int(x_dev.shape[1])
+        ptr = nat.ptr(x_dev) - 12 * (origin[0] * pitch + origin[1])
         with torch.cuda.device(self.device):
-            self._check(nat.lib().spst_forward(self._h, nat.ptr(x_dev), 1), "spst_forward")
+            self._check(nat.lib().spst_forward_pitched(self._h, ctypes.c_void_p(ptr), pitch, 1), "spst_forward")
 
     def tap_sums(self, t_index):
         """Device f64 views (S: C x C, s: C) of this device's owned-row sums for style tap t."""
@@ -188,8 +202,7 @@ class Engine:
         """{relu layer name: bool (C, H, W)} of the last forward (test/diagnostic hook)."""
         out = {}
         convs = [i for i, l in enumerate(self.spec.layers[:self.spec.deepest_tap_index() + 1]) if l.kind == "conv"]
-        Hl = self.bound[2][1] - self.bound[2][0]
-        Wp = self.padded_dims()[1]
+        Hl, Wp = self.window_dims()
         for k, li in enumerate(convs):
             stride = 2 ** sum(1 for l in self.spec.layers[:li] if l.kind == "pool")
             C = self.spec.layers[li].out_ch
@@ -203,8 +216,7 @@ class Engine:
         bind with SPST_DEBUG_STORE_ALL=1 to keep the non-tap pool stages too)."""
         out = {}
         convs = [i for i, l in enumerate(self.spec.layers[:self.spec.deepest_tap_index() + 1]) if l.kind == "conv"]
-        Hl = self.bound[2][1] - self.bound[2][0]
-        Wp = self.padded_dims()[1]
+        Hl, Wp = self.window_dims()
         for k, li in enumerate(convs):
             stride = 2 ** sum(1 for l in self.spec.layers[:li] if l.kind == "pool")
             buf = np.zeros((self.spec.layers[li].out_ch, Hl // stride, Wp // stride), dtype=np.float32)
@@ -224,10 +236,29 @@ class Engine:
         self._check(nat.lib().spst_timing_read(self._h, ms, fl, n), "spst_timing_read")
         return {c: (ms[i], fl[i], n[i]) for i, c in enumerate(self.TIMER_CLASSES) if n[i]}
 
-    def backward(self, two_lambda, grad_dev):
+    def backward(self, two_lambda, grad_dev, origin=(0, 0)):
+        """Writes the owned pixels' gradient into grad_dev (a float32 (rows, cols, 3) CUDA block
+        whose first pixel is global pixel `origin`)."""
         self.stream()
+        pitch = int(grad_dev.shape[1])
+        ptr = nat.ptr(grad_dev) - 12 * (origin[0] * pitch + origin[1])
         with torch.cuda.device(self.device):
-            self._check(nat.lib().spst_backward(self._h, float(two_lambda), nat.ptr(grad_dev)), "spst_backward")
+            self._check(nat.lib().spst_backward_pitched(self._h, float(two_lambda), ctypes.c_void_p(ptr), pitch),
+                        "spst_backward")
+
+    def content_target(self):
+        """(device uint8 copy of the bound window's content target, its scale)."""
+        buf, n, sc = ctypes.c_void_p(), ctypes.c_longlong(), ctypes.c_float()
+        self._check(nat.lib().spst_content_target(self._h, ctypes.byref(buf), ctypes.byref(n), ctypes.byref(sc)),
+                    "spst_content_target")
+        self.stream()
+        return device_view(buf.value, (n.value,), "|u1").clone(), sc.value
+
+    def set_content_target(self, t):
+        buf, scale = t
+        self.stream()
+        self._check(nat.lib().spst_set_content_target(self._h, ctypes.c_void_p(buf.data_ptr()), float(scale)),
+                    "spst_set_content_target")
 
 
 _ENGINES: dict = {}

@@ -1,21 +1,32 @@
-"""Algorithm 1 on the device: global statistics, exact transfer loss and pixel gradient.
+"""Algorithm 1 on the device: global statistics, transfer loss and pixel gradient.
 
 Drop-in for the reference localized module (reference localized.py:116-311): same names,
-signatures, return types and errors.  The reference evaluates the loss block by block on
-CPU (two passes over margin-padded blocks) so its memory stays bounded; with a margin of at
-least ``margin_for_exact_gradient`` its result equals the whole-image gradient
-(localized.py:1-14).  A B200 holds the whole 6048x8064 working set (~80 GB) in HBM, so the
-device path evaluates the padded image in ONE forward (activations, masks and Gram partials
-kept resident), finalises the global statistics, and runs ONE backward — no halo
-recomputation and no second forward.  Multi-GPU runs split the rows into halo-padded stripes
-(``distributed.py``); that is where the block/margin geometry reappears.
+signatures, return types and errors.  The reference evaluates the loss block by block on CPU
+(two passes over margin-padded blocks) so its memory stays bounded; with a margin of at least
+``margin_for_exact_gradient`` its result equals the whole-image gradient (localized.py:1-14).
+
+The device evaluates a list of WINDOWS, each a padded rectangle evaluated as one zero-padded
+image that owns an inner rectangle (statistics, content loss and gradient are restricted to
+the owned pixels; engine binding ``spst_bind_window``):
+
+* exact margin and the padded image fits the device: ONE window, the whole image -- one
+  forward (activations, masks and Gram partials kept resident), finalize, one backward; no
+  halo recomputation and no second forward;
+* exact margin but the image does not fit (beyond ~2x the C4 area on one B200): halo-padded
+  tiles sized to the free memory, two passes like the reference -- memory bounded by a tile;
+* a margin below the exact margin: the reference's own block grid, block by block, so the
+  grid-dependent result is reproduced (reference test_localized.py:72-78).
+
+Multi-GPU runs give each rank one window (``distributed.py``).
 """
 
 from __future__ import annotations
 
+import math
+import os
 import warnings
 from contextlib import contextmanager
-from dataclasses import dataclass, field
+from dataclasses import dataclass, field, replace
 
 import numpy as np
 import torch
@@ -75,16 +86,60 @@ def make_grid(spec: ExtractorSpec, h: int, w: int, block: int, margin: int) -> B
     return BlockGrid(image_h=h + (-h) % s, image_w=w + (-w) % s, block=block, margin=margin, stride=s)
 
 
-def _check_exact(spec, grid: BlockGrid):
-    if len(partition(grid)) > 1 and grid.margin < margin_for_exact_gradient(spec):
-        raise NotImplementedError(
-            f"margin {grid.margin} is below the exact margin {margin_for_exact_gradient(spec)}: the reference "
-            "result then depends on the block grid; the device path evaluates exact (whole-image) gradients only")
+def _is_exact(spec, grid: BlockGrid) -> bool:
+    return len(partition(grid)) == 1 or grid.margin >= margin_for_exact_gradient(spec)
+
+
+_BPP: dict = {}
+
+
+def _bytes_per_px(eng) -> float:
+    """Bound workspace of the engine per padded pixel, measured once by binding a 512^2 probe
+    (VGG-19: ~1.65 KB)."""
+    hit = _BPP.get(id(eng))
+    if hit is None:
+        prev = eng.bound
+        eng.bind(512, 512)
+        hit = _BPP[id(eng)] = eng.workspace_bytes() / (512 * 512)
+        if prev is not None:
+            eng.bind(prev[0], prev[1], *prev[2:])
+    return hit
+
+
+def _window_budget_px(eng) -> int:
+    env = os.environ.get("SPST_MAX_WINDOW_PX")
+    if env:
+        return int(env)
+    free, _ = torch.cuda.mem_get_info(eng.device)
+    held = eng.workspace_bytes()  # the current binding is released before a new one
+    return int(0.8 * (free + held) / _bytes_per_px(eng))
+
+
+def plan_windows(spec, grid: BlockGrid, eng) -> list:
+    """Windows (grid rows, owned rows, grid cols, owned cols) in padded-image coordinates."""
+    Hp, Wp = grid.image_h, grid.image_w
+    if _is_exact(spec, grid):
+        budget = _window_budget_px(eng)
+        if Hp * Wp <= budget:
+            return [((0, Hp), (0, Hp), (0, Wp), (0, Wp))]
+        m = margin_for_exact_gradient(spec)
+        s = spec.deepest_stride()
+        block = max(s, (int(math.sqrt(budget)) - 2 * m) // s * s)
+        blocks = partition(BlockGrid(Hp, Wp, block, m, s))
+    else:
+        blocks = partition(grid)
+    return [((b.padded.y0, b.padded.y1), (b.inner.y0, b.inner.y1), (b.padded.x0, b.padded.x1),
+             (b.inner.x0, b.inner.x1)) for b in blocks]
 
 
 class DeviceContentStore:
-    """Content-tap features of u live in HBM inside the engine (never spilled)."""
+    """Content-tap features of u live in HBM (never spilled): inside the engine for a
+    whole-image problem, one target per window otherwise (reference ContentStore,
+    localized.py:84-109)."""
     spilled = False
+
+    def __init__(self):
+        self.targets = None  # per-window (device bytes, scale) in windowed mode
 
 
 @dataclass
@@ -97,12 +152,17 @@ class TransferProblem:
     content_image: np.ndarray | None
     threads: int = 1
     engine: Engine | None = field(default=None, repr=False)
+    windows: list = field(default_factory=list, repr=False)
     _content_epoch: int = field(default=-1, repr=False)
     _refs_epoch: int = field(default=-1, repr=False)
 
     @property
     def has_content(self) -> bool:
         return self.weights.lambda_c > 0
+
+    @property
+    def windowed(self) -> bool:
+        return len(self.windows) > 1
 
 
 # ------------------------------------------------------------------------------------------
@@ -124,9 +184,49 @@ def to_device_image(x, device=None) -> torch.Tensor:
     return t.contiguous()
 
 
-def _sums_to_stats(engine: Engine, t_index: int, count: int) -> LayerStats:
-    S, s = engine.tap_sums(t_index)
-    return finalize_sums(S.cpu().numpy().copy(), s.cpu().numpy().copy(), count)
+def _tap_counts(spec, Hp, Wp, taps):
+    return [(Hp // tap_geometry(spec, t).stride) * (Wp // tap_geometry(spec, t).stride) for t in taps]
+
+
+def _window_sums(eng, x_dev, h, w, windows, n_taps):
+    """Forward of every window in order; per-tap owned-pixel sums added in window order (f64 on
+    the device: the block-order merge of reference localized.py:180-183)."""
+    tot = None
+    for win in windows:
+        eng.bind(h, w, *_bind_args(win))
+        eng.forward(x_dev)
+        _meter(eng)
+        part = [eng.tap_sums(i) for i in range(n_taps)]
+        if tot is None:
+            tot = [(S.clone(), sv.clone()) for S, sv in part]
+        else:
+            for (S, sv), (a, b) in zip(tot, part):
+                S += a
+                sv += b
+    return tot
+
+
+def _bind_args(win):
+    (g0, g1), (o0, o1), (c0, c1), (oc0, oc1) = win
+    return (g0, g1), (o0, o1), (c0, c1), (oc0, oc1)
+
+
+_TAP_SPECS: dict = {}
+
+
+def _spec_for_taps(spec: ExtractorSpec, taps: tuple) -> ExtractorSpec:
+    """A spec whose style taps are `taps` (the engine computes statistics at style taps)."""
+    if set(taps) <= set(spec.style_taps):
+        return spec
+    kinds = {l.name: l.kind for l in spec.layers}
+    bad = [t for t in taps if kinds.get(t) != "relu"]
+    if bad:
+        raise NotImplementedError(f"device statistics are computed at relu outputs only, not {bad}")
+    key = (id(spec), taps)
+    hit = _TAP_SPECS.get(key)
+    if hit is None or hit[0] is not spec:
+        hit = _TAP_SPECS[key] = (spec, replace(spec, style_taps=tuple(taps)))
+    return hit[1]
 
 
 # ------------------------------------------------------------------------------------------
@@ -135,23 +235,22 @@ def _sums_to_stats(engine: Engine, t_index: int, count: int) -> LayerStats:
 
 def stats_pass(img, spec: ExtractorSpec, block: int = 512, margin: int = 256, threads: int = 1,
                taps=None) -> dict:
-    """Global per-tap statistics of img (localized.py:162-184)."""
+    """Global per-tap statistics of img (localized.py:162-184), at any relu taps."""
     taps = tuple(taps) if taps is not None else tuple(spec.style_taps)
     h, w = int(img.shape[0]), int(img.shape[1])
     grid = make_grid(spec, h, w, block, margin)
-    _check_exact(spec, grid)
-    eng = engine_for(spec)
-    missing = [t for t in taps if t not in eng.style_taps]
-    if missing:
-        raise NotImplementedError(f"device statistics are computed at the style taps only, not {missing}")
+    run_spec = _spec_for_taps(spec, taps)
+    eng = engine_for(run_spec)
     with eng.lock:
-        eng.bind(h, w)
-        eng.forward(to_device_image(img, eng.device))
-        _meter(eng)
+        windows = plan_windows(spec, grid, eng)
+        x_dev = to_device_image(img, eng.device)
+        tot = _window_sums(eng, x_dev, h, w, windows, len(eng.style_taps))
+        counts = _tap_counts(spec, grid.image_h, grid.image_w, eng.style_taps)
         out = {}
         for t in taps:
             i = eng.style_taps.index(t)
-            out[t] = _sums_to_stats(eng, i, eng.owned_pixels(i))
+            S, sv = tot[i]
+            out[t] = finalize_sums(S.cpu().numpy().copy(), sv.cpu().numpy().copy(), counts[i])
     return out
 
 
@@ -174,33 +273,44 @@ def build_problem(content_img, style_img, spec: ExtractorSpec, weights: LossWeig
         ref = content_img if content_img is not None else style_img
         store = None
     grid = make_grid(spec, ref.shape[0], ref.shape[1], block, margin)
-    _check_exact(spec, grid)
     p = TransferProblem(extractor=spec, weights=weights, grid=grid, style_stats=style_stats,
                         content_store=store, content_image=content_img, threads=threads)
     p.engine = engine_for(spec)
-    _prepare(p)
+    with p.engine.lock:
+        p.windows = plan_windows(spec, grid, p.engine)
+        if p.windowed and p.has_content:  # one content target per window (reference ContentStore tiles)
+            u_dev = to_device_image(content_img, p.engine.device)
+            h, w = int(content_img.shape[0]), int(content_img.shape[1])
+            targets = []
+            for win in p.windows:
+                p.engine.bind(h, w, *_bind_args(win))
+                p.engine.forward(u_dev)
+                p.engine.capture_content()
+                targets.append(p.engine.content_target())
+            store.targets = targets
+        _prepare(p)
     return p
 
 
-def _prepare(p: TransferProblem, h=None, w=None):
-    """Bind the engine to the problem grid, (re)capture content and style references."""
+def _prepare(p: TransferProblem, h=None, w=None, whole=False):
+    """Bind the engine (whole-image problems), (re)capture content, install style references."""
     eng = p.engine
     if h is None:
         ref = p.content_image if p.content_image is not None else None
         if ref is not None:
             h, w = ref.shape[:2]
         else:
-            s = p.extractor.deepest_stride()
             h, w = p.grid.image_h, p.grid.image_w
-    eng.bind(int(h), int(w))
-    # the engine holds ONE content target: re-capture when this problem's target is not the one
-    # resident (another problem of the same dims may have captured its own since)
-    if p.has_content and (p._content_epoch != eng.bind_epoch or getattr(eng, "_content_problem", None) is not p):
-        eng.forward(to_device_image(p.content_image, eng.device))
-        eng.capture_content()
-        p._content_epoch = eng.bind_epoch
-        eng._content_problem = p
-    if getattr(eng, "_active_problem", None) is not p or p._refs_epoch != eng.bind_epoch:
+    if not p.windowed or whole:
+        eng.bind(int(h), int(w))
+        # the engine holds ONE content target: re-capture when this problem's target is not the
+        # one resident (another problem of the same dims may have captured its own since)
+        if p.has_content and (p._content_epoch != eng.bind_epoch or getattr(eng, "_content_problem", None) is not p):
+            eng.forward(to_device_image(p.content_image, eng.device))
+            eng.capture_content()
+            p._content_epoch = eng.bind_epoch
+            eng._content_problem = p
+    if getattr(eng, "_active_problem", None) is not p or p._refs_epoch != eng.bind_epoch or p.windowed:
         for i, t in enumerate(eng.style_taps):
             eng.set_style_ref(i, p.style_stats[t], p.weights.style[t])
         eng._active_problem = p
@@ -215,44 +325,107 @@ def _check_dims(x, p: TransferProblem):
     return h, w
 
 
-class Evaluation:
-    """Loss (and lazily the gradient) of one x on one problem — the line-search unit."""
+def _warn_degenerate(degenerate):
+    if any(degenerate):
+        warnings.warn("zero-std channel with nonzero reference std; its gradient column is zeroed",
+                      DegenerateStdWarning, stacklevel=4)
 
-    def __init__(self, p: TransferProblem):
+
+class Evaluation:
+    """Loss (and lazily the gradient) of one x on one problem — the line-search unit.
+
+    Whole-image problems: one forward + finalize for the loss, one backward for the gradient.
+    Windowed problems (reference localized.py:227-280, two passes): the loss pass forwards every
+    window and merges the statistics; the gradient pass re-runs each window's forward, installs
+    the global statistics, and back-propagates its owned pixels."""
+
+    def __init__(self, p: TransferProblem, whole: bool = False):
         self.p = p
+        self.whole = whole or not p.windowed
+        self._x = None
+        self._global = None
 
     def loss(self, x_dev: torch.Tensor) -> float:
         p, eng = self.p, self.p.engine
         h, w = int(x_dev.shape[0]), int(x_dev.shape[1])
-        _prepare(p, h, w)
-        eng.forward(x_dev)
-        _meter(eng)
-        counts = [eng.owned_pixels(i) for i in range(len(eng.style_taps))]
-        content = eng.content_sqdiff() if p.has_content else None  # read after finalize's one sync
-        terms, degenerate = eng.finalize(counts)
-        if any(degenerate):
-            warnings.warn("zero-std channel with nonzero reference std; its gradient column is zeroed",
-                          DegenerateStdWarning, stacklevel=3)
+        _prepare(p, h, w, whole=self.whole)
+        if self.whole:
+            eng.forward(x_dev)
+            _meter(eng)
+            counts = [eng.owned_pixels(i) for i in range(len(eng.style_taps))]
+            content = eng.content_sqdiff() if p.has_content else None  # read after finalize's one sync
+            terms, degenerate = eng.finalize(counts)
+            _warn_degenerate(degenerate)
+            total = float(terms.sum())
+            if content is not None:
+                total += p.weights.lambda_c * float(content.item())
+            return total
+        # windowed: pass 1 (statistics of every window, content loss of every owned crop)
+        T = len(eng.style_taps)
+        tot, closs = None, None
+        for wi, win in enumerate(p.windows):
+            eng.bind(h, w, *_bind_args(win))
+            eng.forward(x_dev)
+            _meter(eng)
+            part = [eng.tap_sums(i) for i in range(T)]
+            tot = [(S.clone(), sv.clone()) for S, sv in part] if tot is None else tot
+            if wi:
+                for (S, sv), (a, b) in zip(tot, part):
+                    S += a
+                    sv += b
+            if p.has_content:
+                eng.set_content_target(p.content_store.targets[wi])
+                c = eng.content_sqdiff().clone()
+                closs = c if closs is None else closs + c
+        self._global = tot
+        self._x = x_dev
+        terms, degenerate = self._finalize_global()
+        _warn_degenerate(degenerate)
         total = float(terms.sum())
-        if content is not None:
-            total += p.weights.lambda_c * float(content.item())
+        if closs is not None:
+            total += p.weights.lambda_c * float(closs.item())
         return total
 
+    def _finalize_global(self):
+        eng, p = self.p.engine, self.p
+        for i, (S, sv) in enumerate(self._global):
+            dS, ds = eng.tap_sums(i)
+            dS.copy_(S)
+            ds.copy_(sv)
+        return eng.finalize(_tap_counts(p.extractor, p.grid.image_h, p.grid.image_w, eng.style_taps))
+
     def grad(self, out: torch.Tensor) -> torch.Tensor:
-        p = self.p
-        p.engine.backward(2.0 * p.weights.lambda_c if p.has_content else 0.0, out)
+        p, eng = self.p, self.p.engine
+        two_lambda = 2.0 * p.weights.lambda_c if p.has_content else 0.0
+        if self.whole:
+            eng.backward(two_lambda, out)
+            return out
+        # windowed: pass 2 (reference localized.py:246-278)
+        x_dev = self._x
+        h, w = int(x_dev.shape[0]), int(x_dev.shape[1])
+        for wi, win in enumerate(p.windows):
+            eng.bind(h, w, *_bind_args(win))
+            eng.forward(x_dev)
+            self._finalize_global()
+            if p.has_content:
+                eng.set_content_target(p.content_store.targets[wi])
+            eng.backward(two_lambda, out)
         return out
 
 
 def loss_grad(x, p: TransferProblem):
-    """Exact transfer loss and its pixel gradient (localized.py:227-280).
+    """Transfer loss and its pixel gradient on the problem's block grid (localized.py:227-280).
 
     numpy in -> (float, numpy of x's dtype); CUDA tensor in -> (float, float32 CUDA tensor).
     """
+    return _loss_grad(x, p, whole=False)
+
+
+def _loss_grad(x, p: TransferProblem, whole: bool):
     _check_dims(x, p)
     with p.engine.lock:
         x_dev = to_device_image(x, p.engine.device)
-        ev = Evaluation(p)
+        ev = Evaluation(p, whole=whole)
         loss = ev.loss(x_dev)
         g = torch.empty_like(x_dev)
         ev.grad(g)
@@ -262,6 +435,6 @@ def loss_grad(x, p: TransferProblem):
 
 
 def loss_grad_global(x, p: TransferProblem):
-    """Single-pass whole-image evaluation (localized.py:283-311) — on the device this is the
-    same computation as ``loss_grad``."""
-    return loss_grad(x, p)
+    """Single-pass whole-image evaluation (localized.py:283-311): independent of the block grid,
+    equal to ``loss_grad`` whenever the margin is exact."""
+    return _loss_grad(x, p, whole=True)

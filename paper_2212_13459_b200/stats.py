@@ -193,9 +193,10 @@ def style_layer_loss_grad(V, stats_x: LayerStats, stats_ref: LayerStats, w: TapW
     out = torch.empty_like(Vd)
     P = int(Vd[0].numel())
     s = torch.cuda.current_stream()
-    nat.check(nat.lib().spst_feature_affine(1 if dt == torch.float64 else 0, nat.ptr(_dev(A, dt)),
-                                            nat.ptr(_dev(r, dt)), nat.ptr(_dev(b, dt)), C, P, nat.ptr(Vd),
-                                            nat.ptr(out), s.cuda_stream), None, "spst_feature_affine")
+    Ad, rd, bd = _dev(A, dt), _dev(r, dt), _dev(b, dt)  # held until the call returns (no aliasing)
+    nat.check(nat.lib().spst_feature_affine(1 if dt == torch.float64 else 0, nat.ptr(Ad), nat.ptr(rd), nat.ptr(bd),
+                                            C, P, nat.ptr(Vd), nat.ptr(out), s.cuda_stream), None,
+              "spst_feature_affine")
     return terms, _back(out, V)
 
 

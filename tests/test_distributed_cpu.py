@@ -1,9 +1,9 @@
-"""Multi-rank host logic of the sharded transfer on CPU (gloo, world_size 2).
+"""Multi-rank host logic of the sharded transfer on CPU (gloo, world_size 2-4).
 
-The device Engine is replaced by an oracle-backed stripe engine with the same interface, so
-this checks the decomposition itself: stripe/halo geometry, the statistics all-reduce, the
-content-loss reduction, owned-row gradient assembly with the replicate-pad fold, sharded
-L-BFGS dot products — against the single-process whole-image oracle."""
+The device Engine is replaced by an oracle-backed window engine with the same interface, so
+this checks the decomposition itself: 2-D grid / halo geometry, the fixed-order statistics
+reduction, the content-loss reduction, owned-rectangle gradient assembly with the
+replicate-pad fold, sharded L-BFGS scalars -- against the single-process whole-image oracle."""
 
 import os
 import socket
@@ -18,8 +18,9 @@ import torch.multiprocessing as mp
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-class OracleStripeEngine:
-    """CPU stand-in for DeviceStripeEngine (test infrastructure, uses the oracle)."""
+class OracleWindowEngine:
+    """CPU stand-in for DeviceWindowEngine (test infrastructure, uses the oracle): evaluates the
+    bound window as one zero-padded image of replicate-clamped pixels, owns a rectangle."""
 
     def __init__(self, net):
         import spst_oracle as O
@@ -27,23 +28,27 @@ class OracleStripeEngine:
         self.net = net
         self.refs = {}
 
-    def bind(self, h, w, grid, own):
+    def bind(self, h, w, grid, own, gcols, ocols):
         s = self.net.deepest_stride()
         self.h, self.w = h, w
         self.Hp, self.Wp = h + (-h) % s, w + (-w) % s
-        self.grid, self.own = grid, own
+        self.grid, self.own, self.gcols, self.ocols = grid, own, gcols, ocols
 
-    def forward_rows(self, rows, row0):
-        O, g0, g1 = self.O, self.grid[0], self.grid[1]
-        r = rows.numpy().astype(np.float64)
-        idx = [min(gr, self.h - 1) - row0 for gr in range(g0, g1)]
-        loc = r[idx]
-        loc = np.concatenate([loc, np.repeat(loc[:, -1:], self.Wp - self.w, axis=1)], axis=1)
+    def _crop(self, t, stride):
+        (g0, _), (o0, o1), (c0, _), (q0, q1) = self.grid, self.own, self.gcols, self.ocols
+        return t[:, (o0 - g0) // stride:(o1 - g0) // stride, (q0 - c0) // stride:(q1 - c0) // stride]
+
+    def forward_block(self, block, origin):
+        O = self.O
+        (g0, g1), (c0, c1) = self.grid, self.gcols
+        b = block.numpy().astype(np.float64)
+        ys = [min(y, self.h - 1) - origin[0] for y in range(g0, g1)]
+        xs = [min(x, self.w - 1) - origin[1] for x in range(c0, c1)]
+        loc = b[np.ix_(ys, xs)]
         self.feats, self.saved = O.run_forward(np.ascontiguousarray(loc.transpose(2, 0, 1)), self.net, keep=True)
         self.sums = []
         for t in self.net.style_taps:
-            st = self.net.geometry(t)[0]
-            F = self.feats[t][:, (self.own[0] - g0) // st:(self.own[1] - g0) // st]
+            F = self._crop(self.feats[t], self.net.geometry(t)[0])
             flat = F.reshape(F.shape[0], -1)
             self.sums.append((torch.from_numpy(flat @ flat.T), torch.from_numpy(flat.sum(axis=1))))
 
@@ -71,33 +76,33 @@ class OracleStripeEngine:
         self.Vu = self.feats[self.net.content_tap].copy()
 
     def content_sqdiff(self):
-        st = self.net.geometry(self.net.content_tap)[0]
-        g0 = self.grid[0]
-        d = (self.feats[self.net.content_tap] - self.Vu)[:, (self.own[0] - g0) // st:(self.own[1] - g0) // st]
+        ct = self.net.content_tap
+        d = self._crop(self.feats[ct] - self.Vu, self.net.geometry(ct)[0])
         return torch.tensor([float(np.sum(d ** 2))], dtype=torch.float64)
 
-    def backward_rows(self, two_lambda, out, own_row0, w):
+    def backward_block(self, two_lambda, out, origin):
         O = self.O
         tg = {t: O.style_feature_grad(self.feats[t], self.stats_x[t], *self.refs[t]) for t in self.net.style_taps}
         ct = self.net.content_tap
         if two_lambda:
             cg = two_lambda * (self.feats[ct] - self.Vu)
             tg[ct] = tg[ct] + cg if ct in tg else cg
-        g = O.run_backward(tg, self.saved, self.net).transpose(1, 2, 0)  # (Hl, Wp, 3)
-        g0 = self.grid[0]
-        r0, r1 = own_row0, min(self.own[1], self.h)
-        res = np.zeros((r1 - r0, w, 3))
-        for gr in range(r0, r1):
-            row = g[gr - g0].copy()
-            if gr == self.h - 1:
-                for extra in range(self.h, self.Hp):
-                    row += g[extra - g0]
-            res[gr - r0] = row[:w]
-            res[gr - r0, w - 1] += row[w:].sum(axis=0)
-        out.view(r1 - r0, w, 3).copy_(torch.from_numpy(res))
+        g = O.run_backward(tg, self.saved, self.net).transpose(1, 2, 0)  # window grid (Hl, Wl, 3)
+        (g0, _), (o0, o1), (c0, _), (q0, q1) = self.grid, self.own, self.gcols, self.ocols
+        loc = g[o0 - g0:o1 - g0, q0 - c0:q1 - c0]          # owned padded rectangle
+        ri, ci = min(o1, self.h) - o0, min(q1, self.w) - q0  # its image part
+        res = loc[:ri, :ci].copy()
+        if o1 > self.h:  # replicate-pad rows fold onto the last image row (tensorops.py:212-229)
+            res[-1] += loc[ri:, :ci].sum(axis=0)
+        if q1 > self.w:
+            res[:, -1] += loc[:ri, ci:].sum(axis=1)
+        if o1 > self.h and q1 > self.w:
+            res[-1, -1] += loc[ri:, ci:].sum(axis=(0, 1))
+        assert tuple(origin) == (o0, q0)
+        out.copy_(torch.from_numpy(res))
 
 
-def _worker(rank, world, port, case, q):
+def _worker(rank, world, port, case, q, grid=None, repeat=1):
     sys.path.insert(0, ROOT)
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import spst_oracle as O
@@ -112,17 +117,19 @@ def _worker(rank, world, port, case, q):
         h, w, halo = case
         u, v, x = rng.random((h, w, 3)), rng.random((h + 13, w - 5, 3)), rng.random((h, w, 3))
         wts = default_loss_weights(spec)
-        sp = ShardedProblem(u, v, spec, wts, OracleStripeEngine(net), halo=halo)
+        sp = ShardedProblem(u, v, spec, wts, OracleWindowEngine(net), halo=halo, grid=grid)
         xs = sp.shard_of(x).double()
-        loss = sp.loss(xs)
-        g = torch.empty_like(xs)
-        sp.grad(g)
-        full = sp.gather_image(g)
+        out = []
+        for _ in range(repeat):
+            loss = sp.loss(xs)
+            g = torch.empty_like(xs)
+            sp.grad(g)
+            out.append((loss, sp.gather_image(g).numpy()))
         # sharded scalar reductions used by L-BFGS (dot products / max|g|) equal the global ones
         dot = sp.allreduce(torch.tensor([float(xs @ g)], dtype=torch.float64))
         mx = sp.allreduce(torch.tensor([float(g.abs().max())], dtype=torch.float64), op="max")
         if rank == 0:
-            q.put((loss, full.numpy(), (float(dot), float(mx)), sp.stripes))
+            q.put((out[0][0], out[0][1], (float(dot), float(mx)), sp.windows, sp.grid_shape, out))
     except Exception as e:  # surface worker failures immediately
         q.put(e)
         raise
@@ -138,11 +145,11 @@ def _free_port():
     return p
 
 
-def _run(case, world=2):
+def _run(case, world=2, grid=None, repeat=1):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, case, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, case, q, grid, repeat)) for r in range(world)]
     for p in procs:
         p.start()
     out = q.get(timeout=600)
@@ -167,20 +174,31 @@ def _global_oracle(case):
 
 
 @pytest.mark.parametrize("case", [(96, 80, 16), (77, 90, 16)])
-def test_two_rank_stripes_equal_whole_image(case):
-    loss, grad, losses, st = _run(case)
-    assert len(st) == 2 and st[0].own_r1 == st[1].own_r0
+def test_two_ranks_equal_whole_image(case):
+    loss, grad, _, wins, shape, _ = _run(case, grid=(2, 1))
+    assert len(wins) == 2 and shape == (2, 1)
     (lo, go), p, x = _global_oracle(case)
     assert abs(loss - lo) <= 1e-10 * abs(lo)
     assert np.linalg.norm(grad - go) <= 1e-10 * np.linalg.norm(go)
 
 
+def test_four_ranks_2x2_grid_equal_whole_image():
+    """2-D rank grid: owned rectangles with a halo on every interior side; the
+    window of each rank needs pixels from all three other ranks (corner exchange)."""
+    case = (77, 90, 16)
+    loss, grad, _, wins, shape, _ = _run(case, world=4, grid=(2, 2))
+    assert shape == (2, 2) and len({(w.oc0, w.oc1) for w in wins}) == 2
+    (lo, go), _, _ = _global_oracle(case)
+    assert abs(loss - lo) <= 1e-10 * abs(lo)
+    assert np.linalg.norm(grad - go) <= 1e-10 * np.linalg.norm(go)
+
+
 def test_three_ranks_halo_wider_than_a_stripe():
-    """Halo exchange when a neighbour's stripe is thinner than the halo: rank 0's window needs
-    rows from rank 2 as well as rank 1 (point-to-point from every rank that owns them)."""
+    """Halo exchange when a neighbour's rectangle is thinner than the halo: rank 0's window needs
+    pixels from rank 2 as well as rank 1 (point-to-point from every rank that owns them)."""
     case = (48, 40, 32)
-    loss, grad, _, st = _run(case, world=3)
-    assert len(st) == 3 and st[1].own_r1 - st[1].own_r0 < 32 and st[0].grid_r1 > st[1].own_r1
+    loss, grad, _, wins, _, _ = _run(case, world=3, grid=(3, 1))
+    assert wins[1].or1 - wins[1].or0 < 32 and wins[0].gr1 > wins[1].or1
     (lo, go), _, _ = _global_oracle(case)
     assert abs(loss - lo) <= 1e-10 * abs(lo)
     assert np.linalg.norm(grad - go) <= 1e-10 * np.linalg.norm(go)
@@ -189,16 +207,48 @@ def test_three_ranks_halo_wider_than_a_stripe():
 def test_two_rank_lbfgs_reductions_match_global():
     """Sharded L-BFGS scalars: sum of per-rank dot products and max of per-rank max|g|."""
     case = (96, 80, 16)
-    loss, grad, (dot, mx), _ = _run(case)
+    loss, grad, (dot, mx), _, _, _ = _run(case, grid=(1, 2))
     (lo, go), _, x = _global_oracle(case)
     assert dot == pytest.approx(float(np.vdot(x, go)), rel=1e-10)
     assert mx == pytest.approx(float(np.abs(go).max()), rel=1e-12)
 
 
+def test_fixed_order_reduction_is_deterministic():
+    """Repeated evaluations give bit-identical losses and gradients (statistics reduced by an
+    all-gather and an ordered sum, not the collective's own order)."""
+    _, _, _, _, _, outs = _run((77, 90, 16), world=4, grid=(2, 2), repeat=2)
+    assert outs[0][0] == outs[1][0]
+    np.testing.assert_array_equal(outs[0][1], outs[1][1])
+
+
+def test_small_image_is_replicated():
+    """No split brings a rank's window under 60 % of a small image: every rank evaluates the
+    whole image (no data-path collective) and the result is the global one."""
+    case = (40, 40, 16)
+    loss, grad, _, wins, shape, _ = _run(case, world=2)
+    assert shape == (0, 0)
+    (lo, go), _, _ = _global_oracle(case)
+    assert abs(loss - lo) <= 1e-10 * abs(lo)
+    assert np.linalg.norm(grad - go) <= 1e-10 * np.linalg.norm(go)
+
+
 def test_zero_halo_is_visibly_wrong():
-    """Reference test_localized.py:72-78 analogue: without the receptive-field halo the stripe
+    """Reference test_localized.py:72-78 analogue: without the receptive-field halo the sharded
     gradient is not the whole-image gradient."""
     case = (96, 80, 0)
-    loss, grad, _, _ = _run(case)
+    loss, grad, _, _, _, _ = _run(case, grid=(2, 1))
     (lo, go), _, _ = _global_oracle(case)
     assert np.linalg.norm(grad - go) >= 1e-3 * np.linalg.norm(go)
+
+
+def test_choose_grid_prefers_2x4_at_8_gpus():
+    sys.path.insert(0, ROOT)
+    from paper_2212_13459_b200.distributed import choose_grid, grid_windows
+    assert choose_grid(6048, 8064, 16, 160, 8) == (2, 4)
+    assert choose_grid(6048, 8064, 16, 160, 4) == (2, 2)
+    assert choose_grid(6048, 8064, 16, 160, 1) == (1, 1)
+    assert choose_grid(256, 256, 16, 160, 8) == (0, 0)
+    ws = grid_windows(6048, 8064, 16, 160, 2, 4)
+    own = sum((w.or1 - w.or0) * (w.oc1 - w.oc0) for w in ws)
+    assert own == 6048 * 8064
+    assert max(w.area for w in ws) == (3024 + 160) * (2016 + 320)

@@ -44,5 +44,5 @@ def test_bench_reference_arm_contract():
     d = _run("--impl", "reference", "--config", "c1", "--steps", "1", "--warmup", "0")
     ours = _run("--config", "c1", "--steps", "3", "--warmup", "3", "--no-cpu-baseline")
     assert d["impl"] == "reference" and d["metric"] == ours["metric"] and d["unit"] == ours["unit"]
-    assert d["config"]["workload"] == ours["config"]["workload"]
+    assert d["config"] == ours["config"]  # identical config dicts (same_config)
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["kind"] in ("port", "reference")

@@ -1,9 +1,11 @@
 """Parity of the device hot path with the reference (golden vectors) and the oracle.
 
-Tolerances (north_star): per-layer Gram and loss within 1e-3 relative; image gradient
-within 1e-3 relative L2 vs the f64 path at the same x.  Where a ReLU-mask flip makes the
-reference's OWN f32 path miss 1e-3 against f64 (a discontinuity of the gradient, SURVEY.md §0
-finding 2), the bar is 1.5x the reference-f32 gap at that x, and the test records it.
+Tolerances (north_star): per-layer Gram and loss within 1e-3 relative; image gradient within
+1e-3 relative L2 vs the f64 path at the same x.  Where a ReLU-mask flip makes the reference's
+OWN f32 path miss 1e-3 against f64 (a discontinuity of the gradient, SURVEY.md §0 finding 2),
+the bar is max(1e-3, 1.5 x the reference-f32 gap at that x); the VGG tests assert exactly
+that, plus fp32-class arithmetic on our own ReLU pattern, and write their per-point tables to
+profiles/.
 """
 
 import numpy as np
@@ -121,41 +123,87 @@ def test_vgg19_style_stats_vs_reference(vgg_spec, vgg_c1):
         assert rel_l2(st[t].gram, d[f"c1_x0_{t}_gram"]) <= 1e-4
 
 
-def test_vgg19_loss_grad_vs_reference_f64(vgg_c1):
+def _table_out(name, rows):
+    """Per-point parity table -> profiles/ (and gpurun_out/ when present, to bring it back)."""
+    import json
+    import os
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for d in ("profiles", "gpurun_out"):
+        path = os.path.join(root, d)
+        if os.path.isdir(path):
+            with open(os.path.join(path, name), "w") as f:
+                json.dump(rows, f, indent=1)
+
+
+def test_vgg19_same_x_gradient_north_star_bar(vgg_spec, vgg_c1):
+    """North-star gradient bar at the reference's own C1 points: x0 = u and its f32 L-BFGS
+    iterates x1..x5 (tests/golden/vgg19_iterates.npz, real reference f64 and f32 gradients).
+
+    * loss within 1e-5 of f64 (north star: 1e-3);
+    * plain image gradient vs f64 within max(1e-3, 1.5 x the reference f32-vs-f64 gap at that x);
+    * arithmetic (f64 network evaluated on OUR ReLU pattern) within 5e-6 -- fp32-class;
+    * every unit whose ReLU sign differs from f64 is a near-tie, |pre| <= 1e-5 rms.
+    """
     d, p = vgg_c1
-    g64 = d["c1_grad64"].astype(np.float64)
-    gap32 = rel_l2(d["c1_grad32"], g64)
-    loss, g = spst.loss_grad(d["c1_u"], p)
-    assert abs(loss - d["c1_loss64"][0]) <= 1e-4 * d["c1_loss64"][0]
-    err = rel_l2(g, g64)
-    # x0 = u sits on many near-zero pre-activations, so the plain comparison is dominated by which
-    # ReLUs flip under fp32-class rounding (the reference's own f32 path is gap32 away from f64).
-    # Arithmetic is checked exactly on our activation pattern, and every flip must be a near-tie.
-    masks = p.engine.relu_masks()
-    net = O.onet_from_spec(p.extractor)
+    it = golden("vgg19_iterates.npz")
+    net = O.onet_from_spec(vgg_spec)
     lam = float(d["c1_lambda_c"][0])
     po = O.build_problem(d["c1_u"].astype(np.float64), d["c1_v"].astype(np.float64), net,
                          O.default_weights(net, lam), 512, 256)
-    _, gm = O.loss_grad_global(d["c1_u"].astype(np.float64), po, masks=masks)
-    arith = rel_l2(g, gm)
-    flips, tie = _flips(masks, _f64_preacts(po, d["c1_u"]))
-    print(f"x0: grad rel-L2 vs f64 {err:.2e} (reference f32 gap {gap32:.2e}); vs f64-on-our-masks {arith:.2e}; "
-          f"ReLU flips {flips} (max |pre|/rms {tie:.1e})")
-    assert arith <= 1e-4
-    assert tie <= 1e-4
-    assert err <= 2e-2
-    # x1: the reference's first line-search trial point (away from x0's near-zero structure)
+    rows = []
+    for k in range(6):
+        x = it[f"x{k}"]
+        loss, g = spst.loss_grad(x, p)
+        g64, g32 = it[f"grad64_{k}"], it[f"grad32_{k}"]
+        l64 = float(it[f"loss64_{k}"][0])
+        masks = p.engine.relu_masks()
+        dead = _degenerate_sets(p, vgg_spec, po, x)
+        _, gm = O.loss_grad_global(x.astype(np.float64), po, masks=masks)
+        flips, tie = _flips(masks, _f64_preacts(po, x))
+        row = dict(point=k, loss_rel=abs(loss - l64) / l64, plain=rel_l2(g, g64), ref_f32_gap=rel_l2(g32, g64),
+                   arith=rel_l2(g, gm), flips=flips, flip_max_pre_over_rms=tie, degenerate=dead)
+        row["bar"] = max(1e-3, 1.5 * row["ref_f32_gap"])
+        rows.append(row)
+        print(f"x{k}: loss rel {row['loss_rel']:.1e}; grad vs f64 {row['plain']:.2e} (bar {row['bar']:.2e}, "
+              f"reference f32 {row['ref_f32_gap']:.2e}); arithmetic {row['arith']:.2e}; flips {flips} "
+              f"(max |pre|/rms {tie:.1e})")
+    _table_out("parity_c1_iterates.json", rows)
+    for r in rows:
+        assert r["loss_rel"] <= 1e-5, r
+        assert r["arith"] <= 5e-6, r
+        assert r["flip_max_pre_over_rms"] <= 1e-5, r
+        assert r["plain"] <= r["bar"], r
+        # the degenerate-std channel sets (stats.py:158-162) are the oracle's, tap by tap
+        for t, (ours, ref) in r["degenerate"].items():
+            assert ours == ref, (r["point"], t, ours, ref)
+
+
+def _degenerate_sets(p, spec, po, x):
+    """{tap: (our channels with std < 1e-8, the f64 oracle's)} at the last forward / at x."""
+    eng = p.engine
+    xp = O.pad_edge16(x.astype(np.float64), po.net.deepest_stride())
+    taps, _ = O.run_forward(np.ascontiguousarray(xp.transpose(2, 0, 1)), po.net)
+    out = {}
+    for i, t in enumerate(eng.style_taps):
+        S, sv = eng.tap_sums(i)
+        ours = spst.stats.finalize_sums(S.cpu().numpy(), sv.cpu().numpy(), eng.owned_pixels(i)).std
+        ref = O.stats_of(taps[t]).std
+        out[t] = (sorted(np.flatnonzero(ours < 1e-8).tolist()), sorted(np.flatnonzero(ref < 1e-8).tolist()))
+    return out
+
+
+def test_vgg19_loss_grad_vs_reference_f64(vgg_c1):
+    """x0 and the steepest-descent trial point x1 of vgg19.npz (reference f64 loss_grad_global)."""
+    d, p = vgg_c1
+    loss, g = spst.loss_grad(d["c1_u"], p)
+    assert abs(loss - d["c1_loss64"][0]) <= 1e-5 * d["c1_loss64"][0]
+    gap32 = rel_l2(d["c1_grad32"], d["c1_grad64"])
+    assert rel_l2(g, d["c1_grad64"]) <= max(1e-3, 1.5 * gap32)
     loss1, g1 = spst.loss_grad(d["c1_x1"], p)
-    assert abs(loss1 - d["c1_loss64_x1"][0]) <= 1e-4 * d["c1_loss64_x1"][0]
-    masks1 = p.engine.relu_masks()
-    _, gm1 = O.loss_grad_global(d["c1_x1"].astype(np.float64), po, masks=masks1)
-    flips1, tie1 = _flips(masks1, _f64_preacts(po, d["c1_x1"]))
-    err1, arith1 = rel_l2(g1, d["c1_grad64_x1"]), rel_l2(g1, gm1)
-    print(f"x1: grad rel-L2 vs f64 {err1:.2e}; vs f64-on-our-masks {arith1:.2e}; ReLU flips {flips1} "
-          f"(max |pre|/rms {tie1:.1e})")
-    assert arith1 <= 1e-4
-    assert tie1 <= 1e-4
-    assert err1 <= 2e-2
+    assert abs(loss1 - d["c1_loss64_x1"][0]) <= 1e-5 * d["c1_loss64_x1"][0]
+    err1 = rel_l2(g1, d["c1_grad64_x1"])
+    print(f"x0: grad vs f64 {rel_l2(g, d['c1_grad64']):.2e} (reference f32 {gap32:.2e}); x1: {err1:.2e}")
+    assert err1 <= 1e-3
 
 
 def test_vgg19_ragged_dims_vs_reference_f64(vgg_spec):
@@ -164,7 +212,7 @@ def test_vgg19_ragged_dims_vs_reference_f64(vgg_spec):
     p = spst.build_problem(d["r_u"], d["r_v"], vgg_spec, w)
     loss, g = spst.loss_grad(d["r_x"], p)
     assert g.shape == (72, 88, 3)
-    assert abs(loss - d["r_loss64"][0]) <= 1e-4 * d["r_loss64"][0]
+    assert abs(loss - d["r_loss64"][0]) <= 1e-5 * d["r_loss64"][0]
     # replicate padding + fold on ragged dims; arithmetic on our ReLU pattern, flips near-ties
     net = O.onet_from_spec(vgg_spec)
     po = O.build_problem(d["r_u"].astype(np.float64), d["r_v"].astype(np.float64), net,
@@ -175,13 +223,13 @@ def test_vgg19_ragged_dims_vs_reference_f64(vgg_spec):
     err, arith = rel_l2(g, d["r_grad64"]), rel_l2(g, gm)
     print(f"ragged: grad rel-L2 vs f64 {err:.2e}; vs f64-on-our-masks {arith:.2e}; ReLU flips {flips} "
           f"(max |pre|/rms {tie:.1e})")
-    assert arith <= 1e-4
-    assert tie <= 1e-4
-    assert err <= 2e-2
+    assert arith <= 5e-6
+    assert tie <= 1e-5
+    assert err <= 1e-3
 
 
 def test_vgg19_lbfgs_same_x_first_five_iterates(vgg_spec, vgg_c1):
-    """Run our L-BFGS 5 iterations; at each of OUR iterates evaluate the f64 oracle (and the
+    """Run OUR L-BFGS 5 iterations; at each of our iterates evaluate the f64 oracle (and the
     oracle's f32 path for the precision envelope) and compare gradients and losses."""
     d, p = vgg_c1
     iterates = []
@@ -194,27 +242,26 @@ def test_vgg19_lbfgs_same_x_first_five_iterates(vgg_spec, vgg_c1):
     po = O.build_problem(d["c1_u"].astype(np.float64), d["c1_v"].astype(np.float64), net,
                          O.default_weights(net, lam), 512, 256)
     po32 = O.build_problem(d["c1_u"], d["c1_v"], net, O.default_weights(net, lam), 512, 256)
+    rows = []
     for it, xi in enumerate(iterates, start=1):
         lo, go = O.loss_grad_global(xi.astype(np.float64), po)
         _, g32 = O.loss_grad_global(xi, po32)
         loss, g = spst.loss_grad(xi, p)
-        # the f64 network evaluated on OUR activation pattern: isolates arithmetic from flips
         masks = p.engine.relu_masks()
         lm, gm = O.loss_grad_global(xi.astype(np.float64), po, masks=masks)
         flips, tie = _flips(masks, _f64_preacts(po, xi))
         err, gap, arith = rel_l2(g, go), rel_l2(g32, go), rel_l2(g, gm)
+        rows.append(dict(iterate=it, loss_rel=abs(loss - lo) / lo, plain=err, oracle_f32_gap=gap, arith=arith,
+                         flips=flips, flip_max_pre_over_rms=tie, bar=max(1e-3, 1.5 * gap)))
         print(f"iterate {it}: loss rel {abs(loss - lo) / lo:.2e}, grad rel-L2 vs f64 {err:.2e} "
               f"(oracle-f32 {gap:.2e}); vs f64-on-our-masks {arith:.2e}; ReLU flips {flips} "
               f"(max |pre|/rms {tie:.1e})")
-        assert abs(loss - lo) <= 1e-4 * lo
-        assert abs(loss - lm) <= 1e-4 * lm
-        assert arith <= 1e-4          # arithmetic: fp32-class
-        # The rest of the plain difference is the ReLU-flip lottery (SURVEY.md §0 finding 2):
-        # every unit whose sign differs from f64 must be a near-tie an fp32-class forward cannot
-        # resolve, and the plain error stays in the range such ties produce (the oracle's own f32
-        # path reaches 6e-3 at these iterates).
-        assert tie <= 1e-4
-        assert err <= 2e-2
+    _table_out("parity_c1_own_iterates.json", rows)
+    for r in rows:
+        assert r["loss_rel"] <= 1e-5, r
+        assert r["arith"] <= 5e-6, r
+        assert r["flip_max_pre_over_rms"] <= 1e-5, r
+        assert r["plain"] <= r["bar"], r
 
 
 def _flips(masks, pre):
@@ -362,3 +409,36 @@ def test_vgg19_five_iterations_final_image(vgg_c1):
     mad = float(np.mean(np.abs(x5 - ref["x5"])))
     print(f"VGG C1 5 iterations: final-image mean |diff| {mad:.2e} (bar {1 / 255:.2e})")
     assert mad <= 1.0 / 255
+
+
+def test_device_nonfinite_keeps_last_x(tiny_spec):
+    """Reference lbfgs.py:92-96 on the DEVICE objective: an evaluation whose activation range
+    cannot be represented (here: an Inf pixel in the trial point) fails inside the native
+    forward with SPST_ERR_NONFINITE; minimize re-raises NonFiniteError carrying the last
+    finite iterate."""
+    rng = np.random.default_rng(3)
+    u, v = (rng.random((48, 48, 3)).astype(np.float32) for _ in range(2))
+    p = spst.build_problem(u, v, tiny_spec, spst.default_loss_weights(tiny_spec), block=64, margin=16)
+    base = objective_for(p)
+    calls = []
+
+    class Poisoned:
+        lazy = True
+
+        def loss(self, x_dev):
+            calls.append(1)
+            if len(calls) == 4:
+                x_dev = x_dev.clone()
+                x_dev[5, 7, 1] = float("inf")
+            return base.loss(x_dev)
+
+        def grad(self, out):
+            return base.grad(out)
+
+    with pytest.raises(spst.NonFiniteError) as ei:
+        spst.minimize(Poisoned(), torch.from_numpy(u).cuda(), spst.LBFGSConfig(max_iters=10))
+    x = ei.value.x
+    assert x is not None and bool(torch.isfinite(torch.as_tensor(x)).all())
+    # the engine is usable afterwards
+    loss, g = spst.loss_grad(u, p)
+    assert np.isfinite(loss) and np.isfinite(g).all()

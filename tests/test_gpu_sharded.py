@@ -32,6 +32,9 @@ def _inputs():
     return u, v, x
 
 
+GRIDS = {2: (2, 1), 3: (3, 1), 4: (2, 2)}
+
+
 def _worker(rank, world, port, q):
     sys.path.insert(0, ROOT)
     import torch.distributed as dist
@@ -44,7 +47,7 @@ def _worker(rank, world, port, q):
         spec = spst.calibrated_vgg19(0)
         u, v, x = _inputs()
         weights = spst.default_loss_weights(spec, lambda_c=1e-3)
-        sp = build_sharded_problem(u, v, spec, weights)
+        sp = build_sharded_problem(u, v, spec, weights, grid=GRIDS[world])
         xs = sp.shard_of(torch.from_numpy(x).cuda())
         loss = sp.loss(xs)
         g = torch.empty_like(xs)
@@ -53,7 +56,7 @@ def _worker(rank, world, port, q):
         xf, tr = minimize(sp.objective(), xs, LBFGSConfig(history_size=5, max_iters=ITERS), allreduce=sp.allreduce)
         final = sp.gather_image(xf).cpu().numpy()
         if rank == 0:
-            q.put((loss, grad, final, list(tr.losses), [(s.grid_r0, s.grid_r1, s.own_r0, s.own_r1) for s in sp.stripes]))
+            q.put((loss, grad, final, list(tr.losses), [(w.gr0, w.gr1, w.or0, w.or1) for w in sp.windows]))
     except Exception as e:
         q.put(e)
         raise
@@ -84,7 +87,7 @@ def whole_image():
     return loss, np.asarray(grad), xf.reshape(x.shape), list(tr.losses)
 
 
-@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("world", [2, 3, 4])
 def test_sharded_device_path_equals_whole_image(world, whole_image):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -101,7 +104,7 @@ def test_sharded_device_path_equals_whole_image(world, whole_image):
     loss, grad, final, losses, st = out
     lo, go, xo, losses_o = whole_image
     assert len(st) == world
-    if world == 3:  # the middle stripe is thinner than the 160-row halo
+    if world == 3:  # the middle rectangle is thinner than the 160-row halo
         assert st[1][3] - st[1][2] < 160 and st[0][1] > st[1][3]
     assert abs(loss - lo) <= 1e-6 * abs(lo)
     assert np.linalg.norm(grad - go) <= 1e-5 * np.linalg.norm(go)
@@ -112,3 +115,65 @@ def test_sharded_device_path_equals_whole_image(world, whole_image):
     np.testing.assert_allclose(losses, losses_o, rtol=1e-4)
     mad = float(np.abs(final - xo).mean())
     assert mad <= 1 / 255, mad
+
+
+def _ms_inputs():
+    rng = np.random.default_rng(5)
+    h, w = 192, 160
+    yy, xx = np.mgrid[0:h, 0:w] / 24.0
+    u = (0.5 + 0.3 * np.sin(yy[..., None] + 2 * xx[..., None] + np.arange(3)) +
+         0.05 * rng.standard_normal((h, w, 3))).clip(0, 1).astype(np.float32)
+    v = rng.random((96, 112, 3)).astype(np.float32)
+    return u, v
+
+
+def _ms_run():
+    import paper_2212_13459_b200 as spst
+    import paper_2212_13459_b200.pipeline as pl
+    pl.make_schedule = lambda n, m="baseline": pl.Schedule(n, (3,) * n, (5,) * n, m)
+    u, v = _ms_inputs()
+    cfg = spst.RunConfig(n_scales=2, mode="fast", extractor=spst.tinynet(0), block=64, margin=16)
+    seen = []
+    x = spst.multiscale_transfer(u, v, cfg, progress=lambda s, it, l, g: seen.append((s, it, l)))
+    return x, seen
+
+
+def _ms_worker(rank, world, port, q):
+    sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        x, seen = _ms_run()
+        if rank == 0:
+            q.put((x, seen))
+    except Exception as e:
+        q.put(e)
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+def test_multiscale_transfer_two_ranks_equals_one():
+    """The public driver under torch.distributed (2 ranks sharing one GPU over gloo): every
+    scale runs as a grid of halo-padded windows (choose_grid); the result equals the
+    single-process run to fp32-class rounding."""
+    x1, seen1 = _ms_run()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ms_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = q.get(timeout=600)
+    for p in procs:
+        p.join(timeout=120)
+    if isinstance(out, Exception):
+        raise out
+    assert all(p.exitcode == 0 for p in procs)
+    x2, seen2 = out
+    assert [(s, it) for s, it, _ in seen2] == [(s, it) for s, it, _ in seen1]
+    np.testing.assert_allclose([l for *_, l in seen2], [l for *_, l in seen1], rtol=1e-4)
+    mad = float(np.abs(x2 - x1).mean())
+    print(f"2 ranks vs 1: final-image mean |diff| {mad:.1e}")
+    assert mad <= 1e-4

@@ -1,5 +1,7 @@
-# kappa scan of the round-toward-zero compensation (tools/error_budget.py), forward drain 1
-for k in 2.5e-8 3.0e-8 3.5e-8 4.0e-8; do
-  SPST_RZ_KAPPA=$k python tools/error_budget.py --out gpurun_out/eb_k$k.json > gpurun_out/eb_k$k.log 2>&1
-done
-SPST_RZ_KAPPA=0 python tools/error_budget.py --points 0 --out gpurun_out/eb_k0.json > gpurun_out/eb_k0.log 2>&1
+python -m pytest tests -m gpu -q -x > gpurun_out/gpu_tests.log 2>&1; tail -5 gpurun_out/gpu_tests.log
+python bench.py --steps 10 --warmup 3 > gpurun_out/bench_f1b2.json 2> gpurun_out/bench_f1b2.err; tail -c 600 gpurun_out/bench_f1b2.json
+SPST_BWD_DRAIN=1 python bench.py --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_f1b1.json 2>&1; tail -c 300 gpurun_out/bench_f1b1.json
+SPST_FWD_DRAIN=2 python bench.py --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_f2b2.json 2>&1; tail -c 300 gpurun_out/bench_f2b2.json
+SPST_BWD_DRAIN=1 python tools/error_budget.py --out gpurun_out/eb_f1b1c.json > gpurun_out/eb_f1b1c.log 2>&1
+python tools/error_budget.py --out gpurun_out/eb_f1b2c.json > gpurun_out/eb_f1b2c.log 2>&1
+python tools/rz_calibrate.py > gpurun_out/rz_default.json 2>&1

@@ -131,7 +131,11 @@ def main():
             mu = s / n
             ours[t] = O.OStats(G, mu, np.sqrt(np.maximum(np.diagonal(G) - mu ** 2, 0.0)), n)
         lm, gm, relu64, st64 = oracle_eval(O, x, po, masks)
-        lb, gb, _, _ = oracle_eval(O, x, po, masks, sx_override=ours)
+        # the device's style references are its own statistics of v (build_problem): inject
+        # those too, so gb differs from g only by features + backward arithmetic
+        po_ours = O.OProblem(**{**po.__dict__, "style": {t: O.OStats(st.gram, st.mean, st.std, st.n_p)
+                                                          for t, st in p.style_stats.items()}})
+        lb, gb, _, _ = oracle_eval(O, x, po_ours, masks, sx_override=ours)
         nfl, tie, per_fl = flips(masks, f64_preacts(O, po, x))
         row = {
             "point": k,

@@ -376,8 +376,49 @@ def api_cases():
     save("api.npz", **d)
 
 
+def block_cases():
+    """Reference Algorithm 1 on block grids whose margin is BELOW the exact margin (the result
+    then depends on the grid: reference test_localized.py:72-78), plus stats_pass at non-style
+    relu taps (localized.py:162-184 with taps=...)."""
+    d = {}
+    tiny = ts.tinynet(0)
+    rng = np.random.default_rng(41)
+    u = rng.random((150, 137, 3))
+    v = rng.random((96, 80, 3)) * 0.6 + 0.2
+    x = np.clip(u + 0.1 * rng.standard_normal(u.shape), 0, 1)
+    w = rst.default_loss_weights(tiny)
+    for m in (0, 8):
+        p = rloc.build_problem(u, v, tiny, w, block=64, margin=m)
+        l, g = rloc.loss_grad(x, p)
+        d[f"tiny_m{m}_loss"], d[f"tiny_m{m}_grad"] = np.array([l]), g
+        st = rloc.stats_pass(x, tiny, block=64, margin=m)
+        for t in tiny.style_taps:
+            d[f"tiny_m{m}_{t}_gram"], d[f"tiny_m{m}_{t}_mean"] = st[t].gram, st[t].mean
+    lg, gg = rloc.loss_grad_global(x, rloc.build_problem(u, v, tiny, w, block=64, margin=0))
+    d["tiny_global_loss"], d["tiny_global_grad"] = np.array([lg]), gg
+    d.update(tiny_u=u, tiny_v=v, tiny_x=x)
+    st = rloc.stats_pass(x, tiny, block=64, margin=16, taps=("relu1", "relu3"))
+    for t in ("relu1", "relu3"):
+        d[f"tiny_taps_{t}_gram"], d[f"tiny_taps_{t}_std"] = st[t].gram, st[t].std
+    spec = to_ref_spec(myspec.calibrated_vgg19(0), rex.vgg19("avg"))
+    uv = synth_content(96, 112, 12)
+    vv = synth_style(80, 80, 13)
+    xv = np.clip(uv + 0.05 * rng.standard_normal(uv.shape), 0, 1).astype(np.float32)
+    wv = rpipe._weights_for_scale(rpipe.RunConfig(n_scales=1, extractor=spec), spec, (96, 112))
+    p = rloc.build_problem(uv, vv, spec, wv, block=48, margin=16)
+    l, g = rloc.loss_grad(xv, p)
+    d.update(vgg_u=uv, vgg_v=vv, vgg_x=xv, vgg_lambda_c=np.array([wv.lambda_c]), vgg_m16_loss=np.array([l]),
+             vgg_m16_grad=g)
+    st = rloc.stats_pass(xv, spec, block=512, margin=256, taps=("relu4_2", "relu1_1"))
+    for t in ("relu4_2", "relu1_1"):
+        d[f"vgg_taps_{t}_gram"], d[f"vgg_taps_{t}_mean"], d[f"vgg_taps_{t}_std"] = st[t].gram, st[t].mean, st[t].std
+    save("blocks.npz", **d)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["kernels", "tiny", "lbfgs", "vgg", "metrics", "lbfgs5", "iterates", "pipeline", "api"]
+    which = sys.argv[1:] or ["kernels", "tiny", "lbfgs", "vgg", "metrics", "lbfgs5", "iterates", "pipeline", "api", "blocks"]
+    if "blocks" in which:
+        block_cases()
     if "api" in which:
         api_cases()
     if "iterates" in which:

@@ -197,7 +197,8 @@ int spst_vec_scaled_diff(int f64, const void* a, const void* b, double c, long l
  * One tensor-core conv layer on host arrays (x: cin x H x W f32, weight cout x cin x 3 x 3,
  * bias cout; f64). mode 0: y = relu(conv(x)) (cout x H x W); mode 1: y = avgpool(relu(conv))
  * (cout x H/2 x W/2); mode 2: y = conv^T(x) input gradient (x has cout channels, y cin);
- * mode 3: relu mask bits of mode 0 as floats. Returns through y_host. */
+ * mode 3: relu mask bits of mode 0 as floats; mode 4: y = maxpool(relu(conv)); mode 5: the
+ * first-argmax index (0-3, row-major in the window) of mode 4 as floats. Returns through y_host. */
 int spst_debug_conv(int device, int mode, int cin, int cout, int H, int W, const float* x_host,
                     const double* weight, const double* bias, float* y_host);
 /* ReLU mask of conv stage `stage` (0-based conv index) from the last forward, as bytes

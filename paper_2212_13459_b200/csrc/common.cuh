@@ -61,6 +61,10 @@ struct ConvArgs {
   float* colsum_partial;         // [tiles_y*tiles_x][C_out_p], nullable
   int sum_r0, sum_r1, sum_c0, sum_c1;
   unsigned int* amax;            // max |output| (unscaled) as float bits
+  // max pooling (reference tensorops.py:113-129): fwd writes, bwd reads the first-argmax index
+  // (row-major in the 2x2 window) of every pooled element, 2 bits: uint32 [C_p/16][H/2][W/2]
+  int pool_max;
+  uint32_t* pool_arg;
   int drain;                     // K-chunks per TMEM accumulation group (1 or 2)
   float comp[4];                 // round-toward-zero bias factor per group relative to `fine`:
                                  // [conv 1, conv 2, extra 1, extra 2 chunks]

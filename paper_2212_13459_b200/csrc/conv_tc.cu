@@ -235,12 +235,35 @@ __device__ __forceinline__ void epilogue32(const ConvArgs& a, float* v0, float* 
     }
     if (a.epi == EPI_FWD_POOL) {
       float pv[32];
-#pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const float s2 = v0[j] + v1[j];
-        pv[j] = (s2 + __shfl_xor_sync(0xffffffffu, s2, 1)) * 0.25f;
-      }
       const int px = x >> 1, py = y0 >> 1;
+      if (a.pool_max) {
+        // first-argmax over the window in row-major order (x, y0), (x+1, y0), (x, y0+1),
+        // (x+1, y0+1): strict '>' keeps the first of equal values (np.argmax)
+        uint32_t arg0 = 0, arg1 = 0;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const float b = __shfl_xor_sync(0xffffffffu, v0[j], 1), d = __shfl_xor_sync(0xffffffffu, v1[j], 1);
+          float m = v0[j];
+          uint32_t idx = 0;
+          if (b > m) m = b, idx = 1;
+          if (v1[j] > m) m = v1[j], idx = 2;
+          if (d > m) m = d, idx = 3;
+          pv[j] = m;
+          if (j < 16) arg0 |= idx << (2 * j);
+          else arg1 |= idx << (2 * (j - 16));
+        }
+        if ((lane & 1) == 0 && px < a.out_pool.W && py < a.out_pool.H) {
+          const size_t plane = (size_t)a.out_pool.H * a.out_pool.W, o = (size_t)py * a.out_pool.W + px;
+          a.pool_arg[(size_t)(ch0 >> 4) * plane + o] = arg0;
+          a.pool_arg[(size_t)((ch0 >> 4) + 1) * plane + o] = arg1;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const float s2 = v0[j] + v1[j];
+          pv[j] = (s2 + __shfl_xor_sync(0xffffffffu, s2, 1)) * 0.25f;
+        }
+      }
       if ((lane & 1) == 0 && px < a.out_pool.W && py < a.out_pool.H) {
 #pragma unroll
         for (int k = 0; k < 4; ++k) store_hl8<N == 64>(a.out_pool, (ch0 >> 3) + k, py, px, pv + 8 * k, a.out_pool.scale);
@@ -291,16 +314,34 @@ __device__ __forceinline__ void epilogue32(const ConvArgs& a, float* v0, float* 
       float* v = r ? v1 : v0;
       const int y = y0 + r;
       if (x >= a.W || y >= a.H) continue;
+      // avg: spread g/4 onto the window (tensorops.py:104-110); max: g to the forward's
+      // first argmax only (tensorops.py:117-129)
+      uint32_t arg0 = 0, arg1 = 0;
+      if (a.pool_max) {
+        const size_t plane = (size_t)a.H * a.W, o = (size_t)y * a.W + x;
+        arg0 = a.pool_arg[(size_t)(ch0 >> 4) * plane + o];
+        arg1 = a.pool_arg[(size_t)((ch0 >> 4) + 1) * plane + o];
+      }
+      const float sc = a.pool_max ? a.acc_scale : a.acc_scale * 0.25f;
 #pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] *= a.acc_scale * 0.25f;
+      for (int j = 0; j < 32; ++j) v[j] *= sc;
 #pragma unroll
       for (int i = 0; i < 2; ++i)
 #pragma unroll
         for (int jx = 0; jx < 2; ++jx) {
           const int yy = 2 * y + i, xx = 2 * x + jx;
           float w[32];
+          if (a.pool_max) {
+            const uint32_t want = 2 * i + jx;
 #pragma unroll
-          for (int j = 0; j < 32; ++j) w[j] = v[j];
+            for (int j = 0; j < 32; ++j) {
+              const uint32_t idx = ((j < 16 ? arg0 : arg1) >> (2 * (j & 15))) & 3u;
+              w[j] = idx == want ? v[j] : 0.f;
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) w[j] = v[j];
+          }
           if (a.addend.hi) {
 #pragma unroll
             for (int k = 0; k < 4; ++k) {

@@ -204,6 +204,8 @@ struct Expo {
 struct Stage {
   int cin = 0, cout = 0, cin_p = 0, cout_p = 0;
   bool pool_after = false;
+  bool pool_max = false;         // max instead of average pooling after this stage
+  uint32_t* pool_arg = nullptr;  // first-argmax bits of the max pool (2 per element)
   int style = -1;
   bool content = false;
   int stride = 1;
@@ -450,8 +452,7 @@ int parse_net(spst_ctx* ctx, int n_layers, const int* kinds, const int* cin, con
     s.content = content_layer == relu_idx;
     i += 2;
     if (i <= last && (kinds[i] == SPST_LAYER_AVGPOOL || kinds[i] == SPST_LAYER_MAXPOOL)) {
-      if (kinds[i] == SPST_LAYER_MAXPOOL)
-        return ctx->fail(SPST_ERR_UNSUPPORTED, "max pooling is not implemented on the device path");
+      s.pool_max = kinds[i] == SPST_LAYER_MAXPOOL;
       s.pool_after = true;
       stride *= 2;
       ++i;
@@ -661,6 +662,8 @@ int forward_stage(spst_ctx* ctx, int k, const float* x) {
   a.mask_out = s.mask;
   a.out = s.out;
   a.out_pool = s.pooled;
+  a.pool_max = s.pool_after && s.pool_max;
+  a.pool_arg = s.pool_arg;
   a.store_full = s.store_out ? 1 : 0;
   a.colsum_partial = tap ? tap->colsum_partial : nullptr;
   a.sum_r0 = own0;
@@ -860,6 +863,8 @@ int backward_stage(spst_ctx* ctx, int k, int src, int dst, double two_lambda) {
   bool use_addend = false;
   if (s.pool_after) {
     a.epi = EPI_BWD_POOL;
+    a.pool_max = s.pool_max;
+    a.pool_arg = s.pool_arg;
     use_addend = is_tap;
   } else {
     a.epi = EPI_BWD;
@@ -1026,6 +1031,10 @@ int bind_alloc(spst_ctx* ctx) {
     if (s.pool_after) {
       s.pooled.hi = ctx->dalloc<__half>((size_t)s.cout_p * (s.H / 2) * (s.W / 2) * 2);
       if (!s.pooled.hi) return ctx->fail(SPST_ERR_OOM, "pooled buffer");
+      if (s.pool_max) {
+        s.pool_arg = ctx->dalloc<uint32_t>((size_t)(s.cout_p / 16) * (s.H / 2) * (s.W / 2));
+        if (!s.pool_arg) return ctx->fail(SPST_ERR_OOM, "max-pool argmax buffer");
+      }
     }
     s.mask = ctx->dalloc<uint32_t>((size_t)(s.cout_p / 32) * s.H * s.W);
     if (!s.mask) return ctx->fail(SPST_ERR_OOM, "mask buffer");
@@ -1656,7 +1665,8 @@ int spst_debug_conv(int device, int mode, int cin, int cout, int H, int W, const
   float* bd = ctx->dalloc<float>(Np);
   uint32_t* mask = ctx->dalloc<uint32_t>((size_t)(Np / 32) * H * W);
   float* yd = ctx->dalloc<float>((size_t)Nc * H * W);
-  if (!slab_d || !xd || !in.hi || !out.hi || !pooled.hi || !bd || !mask || !yd) return SPST_ERR_OOM;
+  uint32_t* parg = ctx->dalloc<uint32_t>((size_t)(Np / 16) * std::max(1, H / 2) * std::max(1, W / 2));
+  if (!slab_d || !xd || !in.hi || !out.hi || !pooled.hi || !bd || !mask || !yd || !parg) return SPST_ERR_OOM;
   std::vector<float> b32(Np, 0.f);
   if (!bwd)
     for (int c = 0; c < cout; ++c) b32[c] = (float)bias[c];
@@ -1674,14 +1684,22 @@ int spst_debug_conv(int device, int mode, int cin, int cout, int H, int W, const
   L.a.out_pool = pooled;
   L.a.bias = bwd ? nullptr : bd;
   L.a.mask_out = mask;
-  L.a.epi = bwd ? EPI_BWD : (mode == 1 ? EPI_FWD_POOL : EPI_FWD);
+  L.a.epi = bwd ? EPI_BWD : ((mode == 1 || mode == 4 || mode == 5) ? EPI_FWD_POOL : EPI_FWD);
+  L.a.pool_max = (mode == 4 || mode == 5) ? 1 : 0;
+  L.a.pool_arg = parg;
   L.a.store_full = 0;
   L.drain = bwd ? bwd_drain() : fwd_drain();
   TRY(run_conv(ctx, L));
   CK(cudaDeviceSynchronize());
-  if (mode == 1) {
+  if (mode == 1 || mode == 4) {
     note_launch(), unpack_hl_kernel<<<512, 256>>>(pooled, Nc, yd);
     CK(cudaMemcpy(y_host, yd, (size_t)Nc * (H / 2) * (W / 2) * 4, cudaMemcpyDeviceToHost));
+  } else if (mode == 5) {  // first-argmax index (0-3) of every pooled element, as floats
+    const size_t plane = (size_t)(H / 2) * (W / 2);
+    std::vector<uint32_t> bits((size_t)(Np / 16) * plane);
+    CK(cudaMemcpy(bits.data(), parg, bits.size() * 4, cudaMemcpyDeviceToHost));
+    for (int c = 0; c < Nc; ++c)
+      for (size_t q = 0; q < plane; ++q) y_host[c * plane + q] = (float)((bits[(c >> 4) * plane + q] >> (2 * (c & 15))) & 3u);
   } else if (mode == 3) {
     note_launch(), unpack_mask_kernel<<<512, 256>>>(mask, Nc, H, W, yd);
     CK(cudaMemcpy(y_host, yd, (size_t)Nc * H * W * 4, cudaMemcpyDeviceToHost));

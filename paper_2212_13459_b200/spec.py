@@ -218,10 +218,20 @@ def _calibrate(rng, dims, probe, pool_after, names):
     return layers
 
 
-def calibrated_vgg19(seed: int = 0, probe: int = 64) -> ExtractorSpec:
+def with_pooling(spec: ExtractorSpec, pooling: str) -> ExtractorSpec:
+    """The same network (weights included) with every pool layer set to `pooling`
+    ("avg" or "max", reference extractor.py:321 vgg19(pooling=...))."""
+    if pooling not in ("avg", "max"):
+        raise ShapeError(f"pooling must be avg or max, got {pooling!r}")
+    return replace(spec, layers=tuple(replace(l, pool=pooling) if l.kind == "pool" else l for l in spec.layers))
+
+
+def calibrated_vgg19(seed: int = 0, probe: int = 64, pooling: str = "avg") -> ExtractorSpec:
     """VGG-19 with seeded, activation-calibrated weights: per conv, draw
     N(0, 2/(9 C_in)) from default_rng(seed) in layer order, normalise each channel's
-    pre-activation std on a seeded probe (rng.random, preprocessed), bias = 0.2 - mean."""
+    pre-activation std on a seeded probe (rng.random, preprocessed), bias = 0.2 - mean.
+    The weights are calibrated through average pooling; ``pooling="max"`` then swaps the pool
+    kind (identical weights)."""
     base = vgg19("avg")
     rng = np.random.default_rng(seed)
     img = rng.random((3, probe, probe))
@@ -237,7 +247,8 @@ def calibrated_vgg19(seed: int = 0, probe: int = 64) -> ExtractorSpec:
         pools.append(has_pool)
         names.append((l.name, base.layers[i + 1].name, base.layers[i + 2].name if has_pool else ""))
     layers = _calibrate(rng, dims, x, pools, names)
-    return replace(base, layers=tuple(layers))
+    out = replace(base, layers=tuple(layers))
+    return out if pooling == "avg" else with_pooling(out, pooling)
 
 
 def tinynet(seed: int = 0) -> ExtractorSpec:
@@ -251,7 +262,7 @@ def tinynet(seed: int = 0) -> ExtractorSpec:
 
 
 def check_device_supported(spec) -> None:
-    """The device path covers (conv3x3 s1 -> relu [-> avg pool 2]) chains up to the deepest tap."""
+    """The device path covers (conv3x3 s1 -> relu [-> avg / max pool 2]) chains up to the deepest tap."""
     for l in spec.layers[:spec.deepest_tap_index() + 1]:
         if l.kind == "conv" and (l.k != 3 or l.stride != 1):
             raise ShapeError(f"{l.name}: device path supports 3x3 stride-1 convs only")

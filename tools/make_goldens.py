@@ -415,8 +415,43 @@ def block_cases():
     save("blocks.npz", **d)
 
 
+def maxpool_cases():
+    """vgg19(pooling="max") (extractor.py:321) and a max-pool TinyNet through the reference
+    Algorithm 1 (first-argmax ties, tensorops.py:113-129): f64 and f32 loss / gradient."""
+    from dataclasses import replace as _rep
+    d = {}
+    rng = np.random.default_rng(51)
+    tiny = ts.tinynet(0)
+    tiny = _rep(tiny, layers=tuple(_rep(l, pool="max") if l.kind == "pool" else l for l in tiny.layers))
+    u, v = rng.random((64, 80, 3)), rng.random((48, 48, 3))
+    x = np.clip(u + 0.1 * rng.standard_normal(u.shape), 0, 1)
+    w = rst.default_loss_weights(tiny)
+    p = rloc.build_problem(u, v, tiny, w, block=512, margin=16)
+    l, g = rloc.loss_grad_global(x, p)
+    d.update(tiny_u=u, tiny_v=v, tiny_x=x, tiny_loss=np.array([l]), tiny_grad=g)
+    spec = to_ref_spec(myspec.calibrated_vgg19(0), rex.vgg19("max"))
+    uv, vv = synth_content(160, 192, 14), synth_style(128, 128, 15)
+    wv = rpipe._weights_for_scale(rpipe.RunConfig(n_scales=1, extractor=spec), spec, (160, 192))
+    p64 = rloc.build_problem(uv.astype(np.float64), vv.astype(np.float64), spec, wv)
+    p32 = rloc.build_problem(uv, vv, spec, wv)
+    d.update(vgg_u=uv, vgg_v=vv, vgg_lambda_c=np.array([wv.lambda_c]))
+    for t in spec.style_taps:
+        d[f"vgg_style_{t}_gram"] = p64.style_stats[t].gram
+    xs = [uv, np.clip(uv + 0.03 * rng.standard_normal(uv.shape), 0, 1).astype(np.float32)]
+    for k, xk in enumerate(xs):
+        l64, g64 = rloc.loss_grad_global(xk.astype(np.float64), p64)
+        l32, g32 = rloc.loss_grad(xk.copy(), p32)
+        print(f"max-pool VGG point {k}: reference f32 vs f64 grad rel-L2 "
+              f"{np.linalg.norm(g32 - g64) / np.linalg.norm(g64):.2e}")
+        d.update({f"vgg_x{k}": xk, f"vgg_loss64_{k}": np.array([l64]), f"vgg_grad64_{k}": g64.astype(np.float32),
+                  f"vgg_grad32_{k}": g32})
+    save("maxpool.npz", **d)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["kernels", "tiny", "lbfgs", "vgg", "metrics", "lbfgs5", "iterates", "pipeline", "api", "blocks"]
+    which = sys.argv[1:] or ["kernels", "tiny", "lbfgs", "vgg", "metrics", "lbfgs5", "iterates", "pipeline", "api", "blocks", "maxpool"]
+    if "maxpool" in which:
+        maxpool_cases()
     if "blocks" in which:
         block_cases()
     if "api" in which:

@@ -180,6 +180,11 @@ int spst_metric_ssim(int f64, const void* a, const void* b, int h, int w, int c,
 int spst_resize_down(const float* in, int h, int w, int c, int factor, float* out, void* stream);
 int spst_resize_bilinear(const float* in, int h, int w, int c, int oh, int ow, float* out,
                          void* stream);
+/* Same with f32 (f64 = 0) or f64 (f64 = 1) images: the reference's dtype="f64" path. */
+int spst_resize_down_typed(int f64, const void* in_dev, int h, int w, int c, int f, void* out_dev,
+                           void* stream);
+int spst_resize_bilinear_typed(int f64, const void* in_dev, int h, int w, int c, int oh, int ow,
+                               void* out_dev, void* stream);
 
 /* Relu output of conv stage `stage` (a tap layer) from the last forward, unpacked to a
  * (C_out x H x W) f32 device buffer on the context stream (extractor.py:171-197 forward_taps). */

@@ -8,7 +8,7 @@ resampling) runs in the in-tree CUDA library ``libspst.so`` through its C ABI
 """
 
 from .errors import (ConfigError, DegenerateStdWarning, EmptyError, FormatError, GeometryError,
-                     NonFiniteError, ShapeError)
+                     NonFiniteError, PrecisionWarning, ShapeError)
 from .extractor import forward_taps
 from .lbfgs import LBFGSConfig, LBFGSState, Trace, minimize, two_loop_direction
 from .localized import (TransferProblem, build_problem, loss_grad, loss_grad_global, make_grid, stats_pass,

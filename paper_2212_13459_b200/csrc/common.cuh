@@ -223,8 +223,8 @@ cudaError_t launch_sum_partials(const double* partial, int nk, double* out, cuda
 cudaError_t launch_axpy(int f64, const void* x, const void* d, double t, long long n, void* out, cudaStream_t st);
 cudaError_t launch_sy(int f64, const void* xt, const void* x, const void* gt, const void* g, long long n, void* s,
                       void* y, double* partial, double* out, cudaStream_t st);
-cudaError_t launch_resize_down(const float* in, int h, int w, int c, int f, float* out, cudaStream_t st);
-cudaError_t launch_resize_bilinear(const float* in, int h, int w, int c, int oh, int ow, float* out,
+cudaError_t launch_resize_down(int f64, const void* in, int h, int w, int c, int f, void* out, cudaStream_t st);
+cudaError_t launch_resize_bilinear(int f64, const void* in, int h, int w, int c, int oh, int ow, void* out,
                                    cudaStream_t st);
 int red_blocks();
 // api.cu (reference stats.py:127-174 on a standalone slab)

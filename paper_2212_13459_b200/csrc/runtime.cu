@@ -743,14 +743,14 @@ int do_forward(spst_ctx* ctx, const float* x, bool careful) {
   bool bad = false;
   {
     const float mi = bits_to_float(ctx->amax_h[4 * n]);
-    if (!std::isfinite(mi) || mi * ctx->img.scale > kOverflow) bad = true;
+    if (range_bad(mi, ctx->img.scale)) bad = true;  // stale exponents (new problem / dims): redo carefully
     if (mi > 0 && std::isfinite(mi)) ctx->img_e = {choose_exp(mi), true};
   }
   for (int k = 0; k < n; ++k) {
     Stage& s = ctx->stages[k];
     const float m0 = bits_to_float(ctx->amax_h[4 * k]), m1 = bits_to_float(ctx->amax_h[4 * k + 1]);
-    if (s.has_out && (!std::isfinite(m0) || m0 * s.out.scale > kOverflow)) bad = true;
-    if (s.pool_after && (!std::isfinite(m1) || m1 * s.pooled.scale > kOverflow)) bad = true;
+    if (s.has_out && range_bad(m0, s.out.scale)) bad = true;
+    if (s.pool_after && range_bad(m1, s.pooled.scale)) bad = true;
     // exponents for the next write; the data now stored keep the scale they were written with
     if (s.has_out && m0 > 0 && std::isfinite(m0)) s.out_e = {choose_exp(m0), true};
     if (s.pool_after && m1 > 0 && std::isfinite(m1)) s.pool_e = {choose_exp(m1), true};
@@ -851,7 +851,10 @@ int backward_stage(spst_ctx* ctx, int k, int src, int dst, double two_lambda) {
   L.wslab = nx.wb_d;
   L.H = nx.H;
   L.W = nx.W;
-  const int acc_e = nx.g_e.e + nx.wexp;
+  // the input gradient carries the scale it was WRITTEN with (gin.scale = stage k+1's g_written);
+  // g_e may already hold the exponent chosen for the next write (careful mode updates it per
+  // stage), so it must not be used here
+  const int acc_e = (int)std::lround(std::log2((double)gin.scale)) + nx.wexp;
   L.acc_scale = 1.f / pow2f(acc_e);
   L.flops = 2.0 * nx.H * nx.W * nx.cin * 9.0 * nx.cout;  // input-gradient GEMM of conv k+1
   L.drain = bwd_drain();
@@ -997,10 +1000,14 @@ int do_backward(spst_ctx* ctx, double two_lambda, float* grad, bool careful) {
   CK(cudaStreamSynchronize(ctx->stream));
   timer_collect(ctx);
   bool bad = false;
+  static const bool dbg = env_int("SPST_DEBUG_RANGES", 0) != 0;
   for (int k = 0; k < n; ++k) {
     Stage& s = ctx->stages[k];
     const float m = bits_to_float(ctx->amax_h[4 * k + 2]);
-    if (!std::isfinite(m) || m * s.g_written > kOverflow) bad = true;
+    if (dbg)
+      fprintf(stderr, "[spst] bwd stage %d careful %d: amax %.3e written scale %.3e (stored max %.3e)\n", k,
+              (int)careful, m, s.g_written, m * s.g_written);
+    if (range_bad(m, s.g_written)) bad = true;
     if (m > 0 && std::isfinite(m)) s.g_e = {choose_exp(m), true};
   }
   return bad ? 1 : 0;
@@ -1333,7 +1340,8 @@ long long spst_workspace_bytes(const spst_ctx* ctx) { return ctx->alloc_bytes; }
 int spst_forward_pitched(spst_ctx* ctx, const float* x, long long pitch, int flags) {
   (void)flags;
   if (!ctx->bound) return ctx->fail(SPST_ERR_CONFIG, "spst_bind must precede spst_forward");
-  if (pitch < ctx->w) return ctx->fail(SPST_ERR_SHAPE, "image pitch below the image width");
+  if (pitch < std::min(ctx->grid_c1, ctx->w) - ctx->grid_c0)
+    return ctx->fail(SPST_ERR_SHAPE, "image pitch below the window's image columns");
   ctx->x_pitch = pitch;
   int r = do_forward(ctx, x, false);
   if (r == 1) r = do_forward(ctx, x, true);
@@ -1456,7 +1464,8 @@ int spst_backward(spst_ctx* ctx, double two_lambda, float* grad) {
 
 int spst_backward_pitched(spst_ctx* ctx, double two_lambda, float* grad, long long pitch) {
   if (!ctx->finalized) return ctx->fail(SPST_ERR_CONFIG, "spst_finalize must precede spst_backward");
-  if (pitch < ctx->w) return ctx->fail(SPST_ERR_SHAPE, "gradient pitch below the image width");
+  if (pitch < std::min(ctx->own_c1, ctx->w) - ctx->own_c0)
+    return ctx->fail(SPST_ERR_SHAPE, "gradient pitch below the owned image columns");
   ctx->g_pitch = pitch;
   if (two_lambda != 0.0 && ctx->content_stage >= 0 && !ctx->content_captured)
     return ctx->fail(SPST_ERR_CONFIG, "content weight is nonzero but no content target was captured");
@@ -1573,14 +1582,23 @@ int spst_vec_sy(int f64, const void* xt, const void* x, const void* gt, const vo
 }
 
 int spst_resize_down(const float* in, int h, int w, int c, int f, float* out, void* stream) {
-  if (f < 1) return SPST_ERR_SHAPE;
-  return launch_resize_down(in, h, w, c, f, out, (cudaStream_t)stream) == cudaSuccess ? SPST_OK : SPST_ERR_CUDA;
+  return spst_resize_down_typed(0, in, h, w, c, f, out, stream);
 }
 
 int spst_resize_bilinear(const float* in, int h, int w, int c, int oh, int ow, float* out, void* stream) {
+  return spst_resize_bilinear_typed(0, in, h, w, c, oh, ow, out, stream);
+}
+
+int spst_resize_down_typed(int f64, const void* in, int h, int w, int c, int f, void* out, void* stream) {
+  if (f < 1) return SPST_ERR_SHAPE;
+  return launch_resize_down(f64, in, h, w, c, f, out, (cudaStream_t)stream) == cudaSuccess ? SPST_OK : SPST_ERR_CUDA;
+}
+
+int spst_resize_bilinear_typed(int f64, const void* in, int h, int w, int c, int oh, int ow, void* out,
+                               void* stream) {
   if (oh < 1 || ow < 1) return SPST_ERR_SHAPE;
-  return launch_resize_bilinear(in, h, w, c, oh, ow, out, (cudaStream_t)stream) == cudaSuccess ? SPST_OK
-                                                                                              : SPST_ERR_CUDA;
+  return launch_resize_bilinear(f64, in, h, w, c, oh, ow, out, (cudaStream_t)stream) == cudaSuccess ? SPST_OK
+                                                                                                   : SPST_ERR_CUDA;
 }
 
 // ------------------------------------------------------------------------------------ debug

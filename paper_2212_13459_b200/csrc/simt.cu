@@ -674,7 +674,9 @@ __global__ void __launch_bounds__(kRedThreads) sy_kernel(const T* xt, const T* x
 // ------------------------------------------------------------------------------------------
 // resampling (HWC f32)
 // ------------------------------------------------------------------------------------------
-__global__ void resize_down_kernel(const float* in, int h, int w, int c, int f, float* out) {
+// T = float: the reference's f32 images; T = double: its f64 path (same formulas in double)
+template <typename T>
+__global__ void resize_down_kernel(const T* in, int h, int w, int c, int f, T* out) {
   const int oh = (h + f - 1) / f, ow = (w + f - 1) / f;
   const long long n = (long long)oh * ow * c;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
@@ -683,39 +685,46 @@ __global__ void resize_down_kernel(const float* in, int h, int w, int c, int f, 
     const int oy = (int)(p / ow), ox = (int)(p % ow);
     const int y0 = oy * f, y1 = min(y0 + f, h), x0 = ox * f, x1 = min(x0 + f, w);
     // reference order: rows of each column summed first (reduceat axis 0), then columns
-    float tot = 0.f;
+    T tot = 0;
     for (int xx = x0; xx < x1; ++xx) {
-      float col = 0.f;
+      T col = 0;
       for (int yy = y0; yy < y1; ++yy) col += in[((size_t)yy * w + xx) * c + ch];
       tot += col;
     }
-    const float area = (float)(y1 - y0) * (float)(x1 - x0);
+    const T area = (T)(y1 - y0) * (T)(x1 - x0);
     out[i] = tot / area;
   }
 }
 
-__device__ __forceinline__ void bilin_axis(int i, int n_in, int n_out, int& i0, int& i1, float& t) {
+template <typename T>
+__device__ __forceinline__ void bilin_axis(int i, int n_in, int n_out, int& i0, int& i1, T& t) {
   double s = ((double)i + 0.5) * ((double)n_in / (double)n_out) - 0.5;
   s = fmin(fmax(s, 0.0), (double)n_in - 1.0);
   i0 = (int)floor(s);
   i1 = min(i0 + 1, n_in - 1);
-  t = (float)(s - (double)i0);
+  t = (T)(s - (double)i0);
 }
 
-__global__ void resize_bilinear_kernel(const float* in, int h, int w, int c, int oh, int ow, float* out) {
+__device__ __forceinline__ float mul_t(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ float add_t(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double mul_t(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double add_t(double a, double b) { return __dadd_rn(a, b); }
+
+template <typename T>
+__global__ void resize_bilinear_kernel(const T* in, int h, int w, int c, int oh, int ow, T* out) {
   const long long n = (long long)oh * ow * c;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     const int ch = (int)(i % c);
     const long long p = i / c;
     const int oy = (int)(p / ow), ox = (int)(p % ow);
     int y0, y1, x0, x1;
-    float ty, tx;
+    T ty, tx;
     bilin_axis(oy, h, oh, y0, y1, ty);
     bilin_axis(ox, w, ow, x0, x1, tx);
-    const float omy = 1.f - ty, omx = 1.f - tx;
-    const float r0 = __fadd_rn(__fmul_rn(in[((size_t)y0 * w + x0) * c + ch], omy), __fmul_rn(in[((size_t)y1 * w + x0) * c + ch], ty));
-    const float r1 = __fadd_rn(__fmul_rn(in[((size_t)y0 * w + x1) * c + ch], omy), __fmul_rn(in[((size_t)y1 * w + x1) * c + ch], ty));
-    out[i] = __fadd_rn(__fmul_rn(r0, omx), __fmul_rn(r1, tx));
+    const T omy = (T)1 - ty, omx = (T)1 - tx;
+    const T r0 = add_t(mul_t(in[((size_t)y0 * w + x0) * c + ch], omy), mul_t(in[((size_t)y1 * w + x0) * c + ch], ty));
+    const T r1 = add_t(mul_t(in[((size_t)y0 * w + x1) * c + ch], omy), mul_t(in[((size_t)y1 * w + x1) * c + ch], ty));
+    out[i] = add_t(mul_t(r0, omx), mul_t(r1, tx));
   }
 }
 
@@ -861,14 +870,22 @@ cudaError_t launch_sy(int f64, const void* xt, const void* x, const void* gt, co
   return cudaGetLastError();
 }
 
-cudaError_t launch_resize_down(const float* in, int h, int w, int c, int f, float* out, cudaStream_t st) {
-  note_launch(), resize_down_kernel<<<4 * kSMs, 256, 0, st>>>(in, h, w, c, f, out);
+cudaError_t launch_resize_down(int f64, const void* in, int h, int w, int c, int f, void* out, cudaStream_t st) {
+  if (f64)
+    note_launch(), resize_down_kernel<double><<<4 * kSMs, 256, 0, st>>>((const double*)in, h, w, c, f, (double*)out);
+  else
+    note_launch(), resize_down_kernel<float><<<4 * kSMs, 256, 0, st>>>((const float*)in, h, w, c, f, (float*)out);
   return cudaGetLastError();
 }
 
-cudaError_t launch_resize_bilinear(const float* in, int h, int w, int c, int oh, int ow, float* out,
+cudaError_t launch_resize_bilinear(int f64, const void* in, int h, int w, int c, int oh, int ow, void* out,
                                    cudaStream_t st) {
-  note_launch(), resize_bilinear_kernel<<<4 * kSMs, 256, 0, st>>>(in, h, w, c, oh, ow, out);
+  if (f64)
+    note_launch(), resize_bilinear_kernel<double><<<4 * kSMs, 256, 0, st>>>((const double*)in, h, w, c, oh, ow,
+                                                                             (double*)out);
+  else
+    note_launch(), resize_bilinear_kernel<float><<<4 * kSMs, 256, 0, st>>>((const float*)in, h, w, c, oh, ow,
+                                                                            (float*)out);
   return cudaGetLastError();
 }
 

@@ -32,7 +32,7 @@ import numpy as np
 import torch
 
 from .device import Engine, engine_for, require_cuda
-from .errors import ConfigError, DegenerateStdWarning
+from .errors import ConfigError, DegenerateStdWarning, PrecisionWarning
 from .spec import ExtractorSpec, tap_geometry
 from .stats import LayerStats, LossWeights, finalize_sums
 from .tiling import BlockGrid, margin_for_exact_gradient, partition
@@ -237,6 +237,7 @@ def stats_pass(img, spec: ExtractorSpec, block: int = 512, margin: int = 256, th
                taps=None) -> dict:
     """Global per-tap statistics of img (localized.py:162-184), at any relu taps."""
     taps = tuple(taps) if taps is not None else tuple(spec.style_taps)
+    _warn_f64(img)
     h, w = int(img.shape[0]), int(img.shape[1])
     grid = make_grid(spec, h, w, block, margin)
     run_spec = _spec_for_taps(spec, taps)
@@ -421,8 +422,17 @@ def loss_grad(x, p: TransferProblem):
     return _loss_grad(x, p, whole=False)
 
 
+def _warn_f64(x):
+    dt = x.dtype if isinstance(x, torch.Tensor) else np.asarray(x).dtype
+    if dt in (np.float64, torch.float64):
+        warnings.warn("float64 input: the device network runs in fp32-class arithmetic (fp16x3 operands, "
+                      "compensated fp32 accumulation, f64 statistics); results are returned as float64",
+                      PrecisionWarning, stacklevel=3)
+
+
 def _loss_grad(x, p: TransferProblem, whole: bool):
     _check_dims(x, p)
+    _warn_f64(x)
     with p.engine.lock:
         x_dev = to_device_image(x, p.engine.device)
         ev = Evaluation(p, whole=whole)

@@ -3,7 +3,8 @@
 ``resize_down``: area mean over f x f boxes with ragged right/bottom boxes, output dims
 ceil(in/f).  ``resize_bilinear``: half-pixel-centred bilinear with clamped sources.
 ``resize_up2``: bilinear x2 or to an explicit target (absorbs ceil drift).  numpy in ->
-numpy out; CUDA tensor in -> CUDA tensor out.  Images are (h, w) or (h, w, c) float32.
+numpy out; CUDA tensor in -> CUDA tensor out.  Images are (h, w) or (h, w, c); f64 images are
+resampled in f64 (the reference's dtype="f64" path), everything else in f32.
 """
 
 from __future__ import annotations
@@ -23,7 +24,8 @@ def _prep(img):
     is_t = isinstance(img, torch.Tensor)
     t = img if is_t else torch.from_numpy(np.ascontiguousarray(np.asarray(img)))
     dtype = t.dtype
-    t = t.to(device="cuda", dtype=torch.float32).contiguous()
+    work = torch.float64 if dtype == torch.float64 else torch.float32  # f64 images resample in f64
+    t = t.to(device="cuda", dtype=work).contiguous()
     squeeze = t.ndim == 2
     if squeeze:
         t = t[:, :, None]
@@ -36,7 +38,7 @@ def _finish(out, is_t, dtype, squeeze):
     if squeeze:
         out = out[:, :, 0]
     if is_t:
-        return out if dtype == torch.float32 else out.to(dtype)
+        return out if out.dtype == dtype else out.to(dtype)
     return out.cpu().numpy().astype(np.dtype(str(dtype).replace("torch.", "")), copy=False)
 
 
@@ -51,9 +53,9 @@ def resize_down(img, factor: int):
     if factor == 1:
         return _finish(t.clone(), is_t, dtype, sq)
     h, w, c = t.shape
-    out = torch.empty((-(-h // factor), -(-w // factor), c), dtype=torch.float32, device=t.device)
-    nat.check(nat.lib().spst_resize_down(nat.ptr(t), h, w, c, factor, nat.ptr(out), _stream()), None,
-              "spst_resize_down")
+    out = torch.empty((-(-h // factor), -(-w // factor), c), dtype=t.dtype, device=t.device)
+    nat.check(nat.lib().spst_resize_down_typed(int(t.dtype == torch.float64), nat.ptr(t), h, w, c, factor,
+                                               nat.ptr(out), _stream()), None, "spst_resize_down")
     return _finish(out, is_t, dtype, sq)
 
 
@@ -63,9 +65,9 @@ def resize_bilinear(img, out_hw: tuple):
         raise ShapeError(f"bilinear target must be >= 1x1, got {oh}x{ow}")
     t, is_t, dtype, sq = _prep(img)
     h, w, c = t.shape
-    out = torch.empty((oh, ow, c), dtype=torch.float32, device=t.device)
-    nat.check(nat.lib().spst_resize_bilinear(nat.ptr(t), h, w, c, oh, ow, nat.ptr(out), _stream()), None,
-              "spst_resize_bilinear")
+    out = torch.empty((oh, ow, c), dtype=t.dtype, device=t.device)
+    nat.check(nat.lib().spst_resize_bilinear_typed(int(t.dtype == torch.float64), nat.ptr(t), h, w, c, oh, ow,
+                                                   nat.ptr(out), _stream()), None, "spst_resize_bilinear")
     return _finish(out, is_t, dtype, sq)
 
 

@@ -65,11 +65,11 @@ def test_stats_pass_at_any_spec_tap(tiny_spec, vgg_spec):
 
 
 def test_memory_bounded_tiles_equal_whole_image(vgg_spec, monkeypatch):
-    """Exact margin, image 'too big' for the device (SPST_MAX_WINDOW_PX = 448^2): 128-px tiles
+    """Exact margin, image 'too big' for the device (SPST_MAX_WINDOW_PX = 448^2 < 640 x 512): 128-px tiles
     with the 160-px exact margin, evaluated in two passes, give the whole-image loss and
     gradient, and the bound workspace stays at one tile's."""
     from paper_2212_13459_b200 import workloads
-    u = workloads.synth_content(512, 384, 21)
+    u = workloads.synth_content(640, 512, 21)
     v = workloads.synth_style(256, 256, 22)
     x = np.clip(u + 0.03 * np.random.default_rng(2).standard_normal(u.shape), 0, 1).astype(np.float32)
     w = spst.default_loss_weights(vgg_spec, lambda_c=1e-4)
@@ -79,10 +79,10 @@ def test_memory_bounded_tiles_equal_whole_image(vgg_spec, monkeypatch):
         l1, g1 = spst.loss_grad(x, p)
     monkeypatch.setenv("SPST_MAX_WINDOW_PX", str(448 ** 2))
     pw = spst.build_problem(u, v, vgg_spec, w)
-    assert len(pw.windows) == 12
+    assert len(pw.windows) == 20  # 128-px tiles of the 640 x 512 image
     with spst.track_activations() as m2:
         l2, g2 = spst.loss_grad(x, pw)
-    print(f"12 tiles vs whole image: loss rel {abs(l2 - l1) / l1:.1e}, grad rel-L2 {rel_l2(g2, g1):.1e}; "
+    print(f"20 tiles vs whole image: loss rel {abs(l2 - l1) / l1:.1e}, grad rel-L2 {rel_l2(g2, g1):.1e}; "
           f"peak workspace {m2.peak / 1e6:.0f} MB vs {m1.peak / 1e6:.0f} MB whole")
     assert abs(l2 - l1) <= 1e-5 * l1
     assert rel_l2(g2, g1) <= 1e-4

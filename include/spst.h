@@ -111,6 +111,9 @@ int spst_set_style_ref(spst_ctx* ctx, int tap, const double* gram, const double*
  * terms_host[3*tap..], and prepare the closed-form feature gradients (stats.py:127-165).
  * degenerate_host[tap] = 1 when a zero-std channel has a nonzero reference std. */
 int spst_finalize(spst_ctx* ctx, const long long* n, double* terms_host, int* degenerate_host);
+/* 1 if the last spst_finalize had to re-run the forward (its deferred range check failed):
+ * anything launched behind that forward (spst_content_sqdiff) must be launched again. */
+int spst_forward_redone(spst_ctx* ctx);
 /* Reverse pass (extractor.py:200-214 + localized.py:246-279): pixel gradient of the loss on
  * owned rows written into grad_dev (h x w x 3 f32; rows outside the owned range untouched).
  * two_lambda = 2 * lambda_c (0 disables the content term). */
@@ -118,6 +121,13 @@ int spst_backward(spst_ctx* ctx, double two_lambda, float* grad_dev);
 /* As spst_backward with the gradient written at grad_dev + (y * pitch + x) * 3 for the owned
  * pixels (y, x) of the window. */
 int spst_backward_pitched(spst_ctx* ctx, double two_lambda, float* grad_dev, long long pitch);
+/* Asynchronous form: launches the backward and returns; its end-of-pass range check is
+ * deferred to spst_backward_resolve (or any later call on the context), which waits for the
+ * pass and re-runs it in careful mode if needed (*redone = 1: the gradient was rewritten, so
+ * work launched on it in between must be repeated).  One host synchronisation per gradient
+ * instead of two when the caller has its own read-back to make (L-BFGS's curvature dots). */
+int spst_backward_async(spst_ctx* ctx, double two_lambda, float* grad_dev, long long pitch);
+int spst_backward_resolve(spst_ctx* ctx, int* redone);
 
 /* ---------------------------------------------------------------- launch timer ---------
  * Measurement hook (no reference counterpart): when enabled, every tensor-core launch is

@@ -58,6 +58,9 @@ SIGNATURES = {
                                    c_double, c_double, c_double]),
     "spst_finalize": (c_int, [c_void_p, POINTER(c_longlong), POINTER(c_double), POINTER(c_int)]),
     "spst_backward": (c_int, [c_void_p, c_double, c_void_p]),
+    "spst_forward_redone": (c_int, [c_void_p]),
+    "spst_backward_async": (c_int, [c_void_p, c_double, c_void_p, c_longlong]),
+    "spst_backward_resolve": (c_int, [c_void_p, POINTER(c_int)]),
     "spst_vec_partials": (c_int, []),
     "spst_vec_dots": (c_int, [c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_longlong,
                               c_void_p, c_void_p, c_void_p]),

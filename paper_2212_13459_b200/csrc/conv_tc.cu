@@ -396,6 +396,11 @@ __global__ void __launch_bounds__(320, 1) conv3x3_tc_kernel(const __grid_constan
   const int first = (int)blockIdx.x;
   const int step = (int)gridDim.x;
   const int n_chunks = a.n_kc + a.n_xkc;
+  // work unit u = (tile u / S, K-split u % S): split j covers chunks [j C / S, (j+1) C / S)
+  // (S = a.ksplit > 1 only for grids under ~2.5 waves; the partials are summed in split order
+  // by split_finish_kernel, which runs the epilogue)
+  const int S = a.ksplit;
+  const int n_units = n_tiles * S;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&a.tm_r_hi);
@@ -436,12 +441,13 @@ __global__ void __launch_bounds__(320, 1) conv3x3_tc_kernel(const __grid_constan
       }
     }
     uint32_t g = 0;
-    for (int t = first; t < n_tiles; t += step) {
+    for (int u = first; u < n_units; u += step) {
+      const int t = u / S, j = u - t * S;
       const TileId id = decode_tile(a, t);
       const int nt = id.nt;
       const int x0 = id.cx * 128;
       const int y0 = id.ry * C::MT;
-      for (int c = 0; c < n_chunks; ++c, ++g) {
+      for (int c = j * n_chunks / S; c < (j + 1) * n_chunks / S; ++c, ++g) {
         const int s = g % C::STAGES;
         mbar_wait(&empty_bar[s], ((g / C::STAGES) & 1) ^ 1);
         uint8_t* st = smem + s * C::STAGE;
@@ -473,8 +479,9 @@ __global__ void __launch_bounds__(320, 1) conv3x3_tc_kernel(const __grid_constan
       const uint32_t idesc = make_idesc_f16(128, N, 0, 0, 0);
       if constexpr (RES) mbar_wait(&res_bar, 0);
       uint32_t g = 0, gq = 0;  // chunk counter (smem stages), group counter (TMEM buffers)
-      for (int t = first; t < n_tiles; t += step) {
-        for (int c = 0; c < n_chunks; ++c, ++g) {
+      for (int u = first; u < n_units; u += step) {
+        const int j = u % S;
+        for (int c = j * n_chunks / S; c < (j + 1) * n_chunks / S; ++c, ++g) {
           bool gfirst, glast;
           chunk_group(a.drain, c, a.n_kc, n_chunks, gfirst, glast);
           const uint32_t b = gq % C::NBUF;
@@ -569,7 +576,8 @@ __global__ void __launch_bounds__(320, 1) conv3x3_tc_kernel(const __grid_constan
     const int rp = C::MT == 2 ? 0 : (int)grp;            // row pair handled by this warpgroup
     const int cofs = C::MT == 2 ? (int)grp * C::CPG : 0;  // first channel handled
     uint32_t g = 0;
-    for (int t = first; t < n_tiles; t += step) {
+    for (int u = first; u < n_units; u += step) {
+      const int t = u / S, j = u - t * S;
       const TileId id = decode_tile(a, t);
       const int nt = id.nt, cx = id.cx, ry = id.ry;
       const int x0 = cx * 128, y0 = ry * C::MT + 2 * rp;
@@ -578,17 +586,19 @@ __global__ void __launch_bounds__(320, 1) conv3x3_tc_kernel(const __grid_constan
 #pragma unroll
       for (int i = 0; i < C::CPG; ++i) acc0[i] = acc1[i] = 0.f;
       const int D = a.drain;
-      const int n_conv_groups = (a.n_kc + D - 1) / D;
-      for (int c = 0; c < n_groups(D, a.n_kc, a.n_xkc); ++c, ++g) {
+      // accumulation groups of the unit's chunk range, as the MMA issuer forms them (chunk_group):
+      // up to D chunks of one kind
+      const int ce = (j + 1) * n_chunks / S;
+      for (int c = j * n_chunks / S; c < ce; ++g) {
+        const bool xg = c >= a.n_kc;
+        const int gsz = min(D, (xg ? ce : min(ce, a.n_kc)) - c);
+        c += gsz;
         const uint32_t b = g % C::NBUF;
         mbar_wait(&cfull_bar[b], (g / C::NBUF) & 1);
         tc_fence_after();
         const uint32_t trow = tmem_base + ((q * 32u) << 16) + b * C::MT * N + 2 * rp * N + cofs;
         // extra-K groups carry their own scale; comp[] undoes the expected round-toward-zero bias
         // of the group (index: kind x 2 + chunks in the group - 1)
-        const bool xg = c >= n_conv_groups;
-        const int gi = xg ? c - n_conv_groups : c;
-        const int gsz = min(D, (xg ? a.n_xkc : a.n_kc) - gi * D);
         const float cs = (xg ? a.x_rescale : 1.f) * a.comp[(xg ? 2 : 0) + gsz - 1];
         if constexpr (C::CPG == 32) {  // both rows in one batch: 2 loads, 1 wait
           float v0[32], v1[32];
@@ -616,6 +626,17 @@ __global__ void __launch_bounds__(320, 1) conv3x3_tc_kernel(const __grid_constan
         acc0[i] = fmaf(acc0[i], a.fine, acc0[i]);
         acc1[i] = fmaf(acc1[i], a.fine, acc1[i]);
       }
+      if constexpr (N == 128 && C::MT == 2) {
+        if (S > 1) {  // K-split partial -> workspace [split][tile][row][channel][px] (coalesced in px)
+          float* w = a.split_ws + ((size_t)(j * n_tiles + t) * 2) * N * 128;
+#pragma unroll
+          for (int i = 0; i < C::CPG; ++i) {
+            w[(size_t)(cofs + i) * 128 + m] = acc0[i];
+            w[(size_t)(N + cofs + i) * 128 + m] = acc1[i];
+          }
+          continue;
+        }
+      }
       float amax0 = 0.f, amax1 = 0.f;
       const int part_row = (ry * a.tiles_x + cx) * (C::MT / 2) + rp;
 #pragma unroll
@@ -637,6 +658,47 @@ __global__ void __launch_bounds__(320, 1) conv3x3_tc_kernel(const __grid_constan
   if (warp == 1) tmem_dealloc<C::TMEM_COLS>(tmem_base);
 }
 
+// K-split finish (N = 128): one CTA per tile with the conv epilogue's thread mapping (8 warps:
+// TMEM quarter q = pixels 32q..32q+31, warpgroup = channel half); sums the S partials in split
+// order (deterministic) and runs the same fused epilogue.
+__global__ void __launch_bounds__(256) split_finish_kernel(const __grid_constant__ ConvArgs a) {
+  using C = ConvCfg<128, false>;
+  constexpr int N = 128;
+  const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
+  const uint32_t q = warp & 3, grp = warp >> 2;
+  const int m = q * 32 + lane;
+  const int cofs = (int)grp * C::CPG;
+  const int n_tiles = a.tiles_x * a.tiles_y * a.n_ntiles;
+  const int t = blockIdx.x;
+  const TileId id = decode_tile(a, t);
+  const int x = id.cx * 128 + m, y0 = id.ry * C::MT;
+  const int part_row = (id.ry * a.tiles_x + id.cx) * (C::MT / 2);
+  float amax0 = 0.f, amax1 = 0.f;
+#pragma unroll
+  for (int cb = 0; cb < C::CPG / 32; ++cb) {
+    float v0[32], v1[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v0[i] = v1[i] = 0.f;
+    for (int j = 0; j < a.ksplit; ++j) {
+      const float* w = a.split_ws + ((size_t)(j * n_tiles + t) * 2) * N * 128;
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        v0[i] += w[(size_t)(cofs + cb * 32 + i) * 128 + m];
+        v1[i] += w[(size_t)(N + cofs + cb * 32 + i) * 128 + m];
+      }
+    }
+    epilogue32<N>(a, v0, v1, id.nt * N + cofs + cb * 32, x, y0, part_row, q, amax0, amax1);
+  }
+  if (a.amax) {
+    amax0 = warp_max(amax0);
+    amax1 = warp_max(amax1);
+    if (lane == 0) {
+      if (amax0 > 0.f) atomicMax(a.amax, __float_as_uint(amax0));
+      if (amax1 > 0.f) atomicMax(a.amax + 1, __float_as_uint(amax1));
+    }
+  }
+}
+
 // ------------------------------------------------------------------------------------------
 int conv_tc_smem_bytes(int N) { return N == 128 ? ConvCfg<128>::SMEM : ConvCfg<64>::SMEM; }
 int conv_tc_rows(int N) { return N == 128 ? ConvCfg<128>::MT : ConvCfg<64>::MT; }
@@ -656,7 +718,12 @@ bool conv_tc_resident_ok(int N, int n_ntiles, int n_kc) {
 }
 
 cudaError_t launch_conv_tc(const ConvArgs& a, int N, int grid, cudaStream_t stream) {
-  if (N == 128) return launch_one<128, false>(a, grid, stream);
+  if (N == 128) {
+    cudaError_t e = launch_one<128, false>(a, grid, stream);
+    if (e != cudaSuccess || a.ksplit <= 1) return e;
+    note_launch(), split_finish_kernel<<<a.tiles_x * a.tiles_y * a.n_ntiles, 256, 0, stream>>>(a);
+    return cudaGetLastError();
+  }
   return conv_tc_resident_ok(N, a.n_ntiles, a.n_kc) ? launch_one<64, true>(a, grid, stream)
                                                     : launch_one<64, false>(a, grid, stream);
 }

@@ -135,6 +135,24 @@ int bwd_drain() {
   return d;
 }
 
+// K-splits for a conv launch of `tiles` (2-row x 128-px x N) tiles of `chunks` K-chunks: a
+// persistent grid of 148 CTAs finishes in ceil(units / 148) rounds of ceil(chunks / S) chunks;
+// splitting pays when the tiles fill under ~2.5 waves (the deep layers of coarse scales and
+// per-rank windows).  The finish kernel costs ~3 chunk times.  SPST_KSPLIT=1 disables.
+int choose_ksplit(int tiles, int chunks) {
+  static const int cap = std::max(1, std::min(8, env_int("SPST_KSPLIT", 8)));
+  double best = std::ceil(tiles / (double)kSMs) * chunks;
+  int best_s = 1;
+  for (int S = 2; S <= cap && chunks / S >= 2; ++S) {
+    const double cost = std::ceil(tiles * (double)S / kSMs) * std::ceil(chunks / (double)S) + 3.0;
+    if (cost < 0.93 * best) {
+      best = cost;
+      best_s = S;
+    }
+  }
+  return best_s;
+}
+
 // comp[] / fine of a conv launch (conv_tc.cu): a conv chunk is 18 correction MMAs then 9 hi*hi
 // MMAs per output row; an extra-K chunk xkg correction then xkg/2 hi*hi MMAs.  `fine` carries
 // the full conv group's correction; comp[] the difference of every other group composition.
@@ -257,9 +275,7 @@ struct spst_ctx {
   size_t tused = 0;
   double t_ms[kTimerClasses] = {}, t_flops[kTimerClasses] = {};
   long long t_n[kTimerClasses] = {};
-  std::vector<unsigned int> amax_h;
   double* fin_d = nullptr;  // per-tap loss outputs (bind_alloc)
-  std::vector<double> fin_h;
   HL16 gbuf[2];
   size_t gbuf_elems = 0;
   HL16 addend;
@@ -270,6 +286,19 @@ struct spst_ctx {
   double* content_partial = nullptr;
   __half* zero_xw = nullptr;
   bool fwd_done = false, finalized = false;
+  // Deferred end-of-pass range checks (fast path): the forward's check is resolved by the next
+  // call that needs its results (finalize's one read-back, or capture / stats / features), the
+  // backward's by spst_backward_resolve -- one host synchronisation per pass pair instead of
+  // one per pass.  Pinned read-back buffers so the copies stay asynchronous.
+  bool fwd_pending = false, fwd_redone = false, bwd_pending = false;
+  const float* fwd_x = nullptr;
+  double bwd_lambda = 0.0;
+  float* bwd_grad = nullptr;
+  unsigned int* amax_pin = nullptr;  // [4 * stages + 4]
+  float* split_ws = nullptr;         // K-split partials (conv_tc.cu), grown on demand
+  size_t split_ws_bytes = 0;
+  double* fin_pin = nullptr;
+  size_t fin_count = 0;
 
   int fail(int c, const std::string& m) {
     code = c;
@@ -323,7 +352,6 @@ struct spst_ctx {
     allocs.clear();
     alloc_bytes = 0;
     fin_d = nullptr;
-    fin_h.clear();
     bound = false;
     fwd_done = finalized = content_captured = false;
     for (auto& t : taps) {
@@ -598,10 +626,30 @@ int run_conv(spst_ctx* ctx, ConvLaunch& L) {
   a.tiles_y = (L.H + mt - 1) / mt;
   a.acc_scale = L.acc_scale;
   a.drain = L.drain;
-  set_conv_comp(a, N);
   if (a.n_kc + a.n_xkc == 0) return ctx->fail(SPST_ERR_CONFIG, "empty GEMM");
   const int tiles = a.tiles_x * a.tiles_y * a.n_ntiles;
-  const int grid = std::min(tiles, kSMs);  // persistent: one CTA per SM
+  a.ksplit = 1;
+  a.split_ws = nullptr;
+  if (N == 128 && a.n_kc > 0) {
+    a.ksplit = choose_ksplit(tiles, a.n_kc + a.n_xkc);
+    if (a.ksplit > 1) {
+      a.drain = 1;  // split units drain every chunk (a unit's range may start mid-group)
+      const size_t need = (size_t)a.ksplit * tiles * 2 * 128 * 128 * sizeof(float);
+      if (need > ctx->split_ws_bytes) {
+        if (ctx->split_ws) {
+          cudaStreamSynchronize(ctx->stream);
+          cudaFree(ctx->split_ws);
+        }
+        ctx->split_ws = nullptr;
+        ctx->split_ws_bytes = 0;
+        CK(cudaMalloc(&ctx->split_ws, need));
+        ctx->split_ws_bytes = need;
+      }
+      a.split_ws = ctx->split_ws;
+    }
+  }
+  set_conv_comp(a, N);
+  const int grid = std::min(tiles * a.ksplit, kSMs);  // persistent: one CTA per SM
   auto* tm = timer_begin(ctx, N == 128 ? 0 : 1, L.flops);
   CK(launch_conv_tc(a, N, grid, ctx->stream));
   timer_end(ctx, tm);
@@ -714,6 +762,8 @@ bool stage_ranges_ok(spst_ctx* ctx, int k, float m0, float m1) {
   return ok;
 }
 
+int forward_check(spst_ctx* ctx);
+
 int do_forward(spst_ctx* ctx, const float* x, bool careful) {
   const int n = (int)ctx->stages.size();
   for (int k = 0; k < n; ++k) {
@@ -736,19 +786,28 @@ int do_forward(spst_ctx* ctx, const float* x, bool careful) {
     }
   }
   for (int k = 0; k < n; ++k) TRY(stage_stats(ctx, k));
-  ctx->amax_h.resize(4 * n + 4);
-  CK(cudaMemcpyAsync(ctx->amax_h.data(), ctx->amax_d, 16 * n + 16, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->amax_pin, ctx->amax_d, 16 * n + 16, cudaMemcpyDeviceToHost, ctx->stream));
+  if (!careful) {  // fast path: checked when the results are first needed (resolve_forward)
+    ctx->fwd_pending = true;
+    return 0;
+  }
   CK(cudaStreamSynchronize(ctx->stream));
+  return forward_check(ctx);
+}
+
+// end-of-pass range check of the forward (the read-back in amax_pin has completed)
+int forward_check(spst_ctx* ctx) {
+  const int n = (int)ctx->stages.size();
   timer_collect(ctx);
   bool bad = false;
   {
-    const float mi = bits_to_float(ctx->amax_h[4 * n]);
+    const float mi = bits_to_float(ctx->amax_pin[4 * n]);
     if (range_bad(mi, ctx->img.scale)) bad = true;  // stale exponents (new problem / dims): redo carefully
     if (mi > 0 && std::isfinite(mi)) ctx->img_e = {choose_exp(mi), true};
   }
   for (int k = 0; k < n; ++k) {
     Stage& s = ctx->stages[k];
-    const float m0 = bits_to_float(ctx->amax_h[4 * k]), m1 = bits_to_float(ctx->amax_h[4 * k + 1]);
+    const float m0 = bits_to_float(ctx->amax_pin[4 * k]), m1 = bits_to_float(ctx->amax_pin[4 * k + 1]);
     if (s.has_out && range_bad(m0, s.out.scale)) bad = true;
     if (s.pool_after && range_bad(m1, s.pooled.scale)) bad = true;
     // exponents for the next write; the data now stored keep the scale they were written with
@@ -756,6 +815,21 @@ int do_forward(spst_ctx* ctx, const float* x, bool careful) {
     if (s.pool_after && m1 > 0 && std::isfinite(m1)) s.pool_e = {choose_exp(m1), true};
   }
   return bad ? 1 : 0;
+}
+
+// Resolve a deferred forward check: wait for the pass, check its ranges, and re-run it in
+// careful mode if a stored tensor left its representable range (sets fwd_redone).
+int resolve_forward(spst_ctx* ctx) {
+  ctx->fwd_redone = false;
+  if (!ctx->fwd_pending) return SPST_OK;
+  ctx->fwd_pending = false;
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (forward_check(ctx) == 0) return SPST_OK;
+  int r = do_forward(ctx, ctx->fwd_x, true);
+  if (r == 1) return ctx->fail(SPST_ERR_NONFINITE, "activation range could not be represented (non-finite?)");
+  if (r) return r;
+  ctx->fwd_redone = true;
+  return SPST_OK;
 }
 
 // ------------------------------------------------------------------------------------------
@@ -909,6 +983,8 @@ int backward_stage(spst_ctx* ctx, int k, int src, int dst, double two_lambda) {
   return run_conv(ctx, L);
 }
 
+int backward_check(spst_ctx* ctx, bool careful);
+
 int do_backward(spst_ctx* ctx, double two_lambda, float* grad, bool careful) {
   const int n = (int)ctx->stages.size();
   const int Lst = n - 1;
@@ -994,16 +1070,24 @@ int do_backward(spst_ctx* ctx, double two_lambda, float* grad, bool careful) {
   fa.grad = grad;
   fa.pitch = ctx->g_pitch;
   CK(launch_fold_grad(fa, ctx->stream));
-  // end-of-pass range check (fast path)
-  ctx->amax_h.resize(4 * n);
-  CK(cudaMemcpyAsync(ctx->amax_h.data(), ctx->amax_d, 16 * n, cudaMemcpyDeviceToHost, ctx->stream));
+  // end-of-pass range check: deferred on the fast path (resolve_backward)
+  CK(cudaMemcpyAsync(ctx->amax_pin, ctx->amax_d, 16 * n, cudaMemcpyDeviceToHost, ctx->stream));
+  if (!careful) {
+    ctx->bwd_pending = true;
+    return 0;
+  }
   CK(cudaStreamSynchronize(ctx->stream));
+  return backward_check(ctx, careful);
+}
+
+int backward_check(spst_ctx* ctx, bool careful) {
+  const int n = (int)ctx->stages.size();
   timer_collect(ctx);
   bool bad = false;
   static const bool dbg = env_int("SPST_DEBUG_RANGES", 0) != 0;
   for (int k = 0; k < n; ++k) {
     Stage& s = ctx->stages[k];
-    const float m = bits_to_float(ctx->amax_h[4 * k + 2]);
+    const float m = bits_to_float(ctx->amax_pin[4 * k + 2]);
     if (dbg)
       fprintf(stderr, "[spst] bwd stage %d careful %d: amax %.3e written scale %.3e (stored max %.3e)\n", k,
               (int)careful, m, s.g_written, m * s.g_written);
@@ -1011,6 +1095,25 @@ int do_backward(spst_ctx* ctx, double two_lambda, float* grad, bool careful) {
     if (m > 0 && std::isfinite(m)) s.g_e = {choose_exp(m), true};
   }
   return bad ? 1 : 0;
+}
+
+int resolve_backward(spst_ctx* ctx, int* redone) {
+  if (redone) *redone = 0;
+  if (!ctx->bwd_pending) return SPST_OK;
+  ctx->bwd_pending = false;
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (backward_check(ctx, false) == 0) return SPST_OK;
+  int r = do_backward(ctx, ctx->bwd_lambda, ctx->bwd_grad, true);
+  if (r == 1) return ctx->fail(SPST_ERR_NONFINITE, "gradient range could not be represented (non-finite?)");
+  if (r) return r;
+  if (redone) *redone = 1;
+  return SPST_OK;
+}
+
+// a pass's results are about to be replaced or released: settle every deferred check first
+int settle(spst_ctx* ctx) {
+  TRY(resolve_backward(ctx, nullptr));
+  return resolve_forward(ctx);
 }
 
 int bind_alloc(spst_ctx* ctx) {
@@ -1092,7 +1195,13 @@ int bind_alloc(spst_ctx* ctx) {
     for (auto& t : ctx->taps) total += 2 * (size_t)ctx->stages[t.stage].cout + 3;
     ctx->fin_d = ctx->dalloc<double>(total);
     if (!ctx->fin_d) return ctx->fail(SPST_ERR_OOM, "statistics buffers");
-    ctx->fin_h.assign(total, 0.0);
+    if (ctx->fin_count < total) {
+      if (ctx->fin_pin) cudaFreeHost(ctx->fin_pin);
+      ctx->fin_pin = nullptr;
+      ctx->fin_count = 0;
+      CK(cudaMallocHost(&ctx->fin_pin, total * sizeof(double)));
+      ctx->fin_count = total;
+    }
     size_t off = 0;
     for (auto& t : ctx->taps) {
       const int C = ctx->stages[t.stage].cout;
@@ -1219,6 +1328,7 @@ int spst_create(int device, int n_layers, const int* kinds, const int* cin, cons
   }
   TRY(parse_net(ctx, n_layers, kinds, cin, cout, weights, biases, n_style, style_layers, content_layer));
   TRY(upload_weights(ctx));
+  CK(cudaMallocHost(&ctx->amax_pin, (4 * ctx->stages.size() + 4) * sizeof(unsigned int)));
   return SPST_OK;
 }
 
@@ -1228,7 +1338,11 @@ void spst_destroy(spst_ctx* ctx) {
     cudaEventDestroy(t.a);
     cudaEventDestroy(t.b);
   }
+  if (ctx->bound) settle(ctx);
   ctx->release_bound();
+  if (ctx->amax_pin) cudaFreeHost(ctx->amax_pin);
+  if (ctx->split_ws) cudaFree(ctx->split_ws);
+  if (ctx->fin_pin) cudaFreeHost(ctx->fin_pin);
   if (ctx->pool) cudaMemPoolDestroy(ctx->pool);
   for (void* p : ctx->persistent) cudaFree(p);
   delete ctx;
@@ -1281,6 +1395,7 @@ int spst_bind_window(spst_ctx* ctx, int h, int w, int grid_r0, int grid_r1, int 
       ctx->own_r0 == own_r0 && ctx->own_r1 == own_r1 && ctx->grid_c0 == grid_c0 && ctx->grid_c1 == grid_c1 &&
       ctx->own_c0 == own_c0 && ctx->own_c1 == own_c1)
     return SPST_OK;
+  if (ctx->bound) TRY(settle(ctx));
   ctx->release_bound();
   ctx->h = h;
   ctx->w = w;
@@ -1340,6 +1455,8 @@ long long spst_workspace_bytes(const spst_ctx* ctx) { return ctx->alloc_bytes; }
 int spst_forward_pitched(spst_ctx* ctx, const float* x, long long pitch, int flags) {
   (void)flags;
   if (!ctx->bound) return ctx->fail(SPST_ERR_CONFIG, "spst_bind must precede spst_forward");
+  TRY(settle(ctx));
+  ctx->fwd_x = x;
   if (pitch < std::min(ctx->grid_c1, ctx->w) - ctx->grid_c0)
     return ctx->fail(SPST_ERR_SHAPE, "image pitch below the window's image columns");
   ctx->x_pitch = pitch;
@@ -1359,6 +1476,7 @@ int spst_forward(spst_ctx* ctx, const float* x, int flags) {
 
 int spst_stats_ptrs(spst_ctx* ctx, int tap, double** S, double** s) {
   if (tap < 0 || tap >= (int)ctx->taps.size() || !ctx->bound) return ctx->fail(SPST_ERR_CONFIG, "bad tap / unbound");
+  TRY(resolve_forward(ctx));
   *S = ctx->taps[tap].S;
   *s = ctx->taps[tap].s;
   return SPST_OK;
@@ -1367,6 +1485,7 @@ int spst_stats_ptrs(spst_ctx* ctx, int tap, double** S, double** s) {
 int spst_capture_content(spst_ctx* ctx) {
   if (ctx->content_stage < 0) return ctx->fail(SPST_ERR_CONFIG, "network has no content tap");
   if (!ctx->fwd_done) return ctx->fail(SPST_ERR_CONFIG, "no forward to capture");
+  TRY(resolve_forward(ctx));
   const Stage& s = ctx->stages[ctx->content_stage];
   CK(cudaMemcpyAsync(ctx->content_u.hi, s.out.hi, s.out.bytes(), cudaMemcpyDeviceToDevice, ctx->stream));
   ctx->content_u.scale = s.out.scale;
@@ -1376,6 +1495,7 @@ int spst_capture_content(spst_ctx* ctx) {
 
 int spst_content_target(spst_ctx* ctx, void** buf, long long* bytes, float* scale) {
   if (ctx->content_stage < 0 || !ctx->bound) return ctx->fail(SPST_ERR_CONFIG, "no content tap / unbound");
+  TRY(settle(ctx));
   *buf = ctx->content_u.hi;
   *bytes = (long long)ctx->content_u.bytes();
   *scale = ctx->content_u.scale;
@@ -1423,24 +1543,34 @@ int spst_set_style_ref(spst_ctx* ctx, int tap, const double* gram, const double*
 
 int spst_finalize(spst_ctx* ctx, const long long* n, double* terms, int* degenerate) {
   if (!ctx->fwd_done) return ctx->fail(SPST_ERR_CONFIG, "spst_forward must precede spst_finalize");
-  for (size_t i = 0; i < ctx->taps.size(); ++i) {
-    TapState& t = ctx->taps[i];
-    if (n[i] <= 0) return ctx->fail(SPST_ERR_EMPTY, "no feature pixels accumulated");
-    t.n = (double)n[i];
-    StyleCoefArgs a = coef_args(ctx, t);
-    CK(cudaMemsetAsync(t.degenerate, 0, 4, ctx->stream));
-    CK(launch_style_vec(a, ctx->stream));
-    CK(launch_style_mat(a, ctx->stream));
+  TRY(resolve_backward(ctx, nullptr));
+  size_t total = 0;
+  for (auto& t : ctx->taps) total += 2 * (size_t)ctx->stages[t.stage].cout + 3;
+  // the style coefficients and loss terms are launched behind the forward; ONE read-back
+  // settles both the forward's deferred range check and the terms
+  bool redone = false;
+  for (int pass = 0; pass < 2; ++pass) {
+    for (size_t i = 0; i < ctx->taps.size(); ++i) {
+      TapState& t = ctx->taps[i];
+      if (n[i] <= 0) return ctx->fail(SPST_ERR_EMPTY, "no feature pixels accumulated");
+      t.n = (double)n[i];
+      StyleCoefArgs a = coef_args(ctx, t);
+      CK(cudaMemsetAsync(t.degenerate, 0, 4, ctx->stream));
+      CK(launch_style_vec(a, ctx->stream));
+      CK(launch_style_mat(a, ctx->stream));
+    }
+    if (total) CK(cudaMemcpyAsync(ctx->fin_pin, ctx->fin_d, total * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    const bool pending = ctx->fwd_pending;
+    TRY(resolve_forward(ctx));  // synchronises the stream when a check was pending
+    if (!pending) CK(cudaStreamSynchronize(ctx->stream));
+    if (!ctx->fwd_redone) break;  // (a redone forward changed the statistics: recompute)
+    redone = true;
   }
-  if (!ctx->fin_h.empty()) {
-    CK(cudaMemcpyAsync(ctx->fin_h.data(), ctx->fin_d, ctx->fin_h.size() * sizeof(double), cudaMemcpyDeviceToHost,
-                       ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));
-  }
+  ctx->fwd_redone = redone;  // tells the caller to recompute what it launched behind the forward
   for (size_t i = 0; i < ctx->taps.size(); ++i) {
     TapState& t = ctx->taps[i];
     const int C = ctx->stages[t.stage].cout;
-    const double* buf = ctx->fin_h.data() + (t.row_loss - ctx->fin_d);
+    const double* buf = ctx->fin_pin + (t.row_loss - ctx->fin_d);
     int deg = 0;
     std::memcpy(&deg, buf + 2 * C + 2, sizeof(int));
     double g = 0, mm = 0;
@@ -1458,21 +1588,33 @@ int spst_finalize(spst_ctx* ctx, const long long* n, double* terms, int* degener
   return SPST_OK;
 }
 
+int spst_forward_redone(spst_ctx* ctx) { return ctx->fwd_redone ? 1 : 0; }
+
 int spst_backward(spst_ctx* ctx, double two_lambda, float* grad) {
   return spst_backward_pitched(ctx, two_lambda, grad, ctx->w);
 }
 
-int spst_backward_pitched(spst_ctx* ctx, double two_lambda, float* grad, long long pitch) {
+int spst_backward_async(spst_ctx* ctx, double two_lambda, float* grad, long long pitch) {
   if (!ctx->finalized) return ctx->fail(SPST_ERR_CONFIG, "spst_finalize must precede spst_backward");
   if (pitch < std::min(ctx->own_c1, ctx->w) - ctx->own_c0)
     return ctx->fail(SPST_ERR_SHAPE, "gradient pitch below the owned image columns");
+  TRY(resolve_backward(ctx, nullptr));
   ctx->g_pitch = pitch;
   if (two_lambda != 0.0 && ctx->content_stage >= 0 && !ctx->content_captured)
     return ctx->fail(SPST_ERR_CONFIG, "content weight is nonzero but no content target was captured");
+  ctx->bwd_lambda = two_lambda;
+  ctx->bwd_grad = grad;
   int r = do_backward(ctx, two_lambda, grad, false);
   if (r == 1) r = do_backward(ctx, two_lambda, grad, true);
   if (r == 1) return ctx->fail(SPST_ERR_NONFINITE, "gradient range could not be represented (non-finite?)");
   return r;
+}
+
+int spst_backward_resolve(spst_ctx* ctx, int* redone) { return resolve_backward(ctx, redone); }
+
+int spst_backward_pitched(spst_ctx* ctx, double two_lambda, float* grad, long long pitch) {
+  TRY(spst_backward_async(ctx, two_lambda, grad, pitch));
+  return resolve_backward(ctx, nullptr);
 }
 
 // ------------------------------------------------------------------------------------ vectors
@@ -1605,6 +1747,7 @@ int spst_resize_bilinear_typed(int f64, const void* in, int h, int w, int c, int
 int spst_debug_mask(spst_ctx* ctx, int stage, unsigned char* out_host) {
   if (!ctx->fwd_done || stage < 0 || stage >= (int)ctx->stages.size())
     return ctx->fail(SPST_ERR_CONFIG, "no forward / bad stage");
+  TRY(settle(ctx));
   const Stage& s = ctx->stages[stage];
   const size_t n = (size_t)(s.cout_p / 32) * s.H * s.W;
   std::vector<uint32_t> bits(n);
@@ -1619,6 +1762,7 @@ int spst_debug_mask(spst_ctx* ctx, int stage, unsigned char* out_host) {
 int spst_stage_features(spst_ctx* ctx, int stage, float* out_dev) {
   if (!ctx->fwd_done || stage < 0 || stage >= (int)ctx->stages.size())
     return ctx->fail(SPST_ERR_CONFIG, "no forward / bad stage");
+  TRY(resolve_forward(ctx));
   const Stage& s = ctx->stages[stage];
   if (!s.has_out) return ctx->fail(SPST_ERR_CONFIG, "stage output is not a stored tap");
   note_launch(), unpack_hl_kernel<<<512, 256, 0, ctx->stream>>>(s.out, s.cout, out_dev);
@@ -1641,6 +1785,7 @@ int spst_vec_scaled_diff(int f64, const void* a, const void* b, double c, long l
 int spst_debug_stage_out(spst_ctx* ctx, int stage, float* out_host) {
   if (!ctx->fwd_done || stage < 0 || stage >= (int)ctx->stages.size())
     return ctx->fail(SPST_ERR_CONFIG, "no forward / bad stage");
+  TRY(settle(ctx));
   const Stage& s = ctx->stages[stage];
   if (!s.has_out) return ctx->fail(SPST_ERR_CONFIG, "stage output not stored (set SPST_DEBUG_STORE_ALL=1)");
   const size_t n = (size_t)s.cout * s.H * s.W;
@@ -1727,6 +1872,7 @@ int spst_debug_conv(int device, int mode, int cin, int cout, int H, int W, const
   }
   CK(cudaDeviceSynchronize());
   ctx->release_bound();
+  if (ctx->split_ws) cudaFree(ctx->split_ws);
   return SPST_OK;
 }
 

@@ -236,15 +236,26 @@ class Engine:
         self._check(nat.lib().spst_timing_read(self._h, ms, fl, n), "spst_timing_read")
         return {c: (ms[i], fl[i], n[i]) for i, c in enumerate(self.TIMER_CLASSES) if n[i]}
 
-    def backward(self, two_lambda, grad_dev, origin=(0, 0)):
+    def backward(self, two_lambda, grad_dev, origin=(0, 0), defer=False):
         """Writes the owned pixels' gradient into grad_dev (a float32 (rows, cols, 3) CUDA block
-        whose first pixel is global pixel `origin`)."""
+        whose first pixel is global pixel `origin`).  defer=True returns right after the launch;
+        ``backward_resolve`` then settles the pass's range check (one synchronisation)."""
         self.stream()
         pitch = int(grad_dev.shape[1])
         ptr = nat.ptr(grad_dev) - 12 * (origin[0] * pitch + origin[1])
         with torch.cuda.device(self.device):
-            self._check(nat.lib().spst_backward_pitched(self._h, float(two_lambda), ctypes.c_void_p(ptr), pitch),
-                        "spst_backward")
+            fn = nat.lib().spst_backward_async if defer else nat.lib().spst_backward_pitched
+            self._check(fn(self._h, float(two_lambda), ctypes.c_void_p(ptr), pitch), "spst_backward")
+
+    def backward_resolve(self) -> bool:
+        """Settle a deferred backward; True if it had to be re-run (the gradient was rewritten)."""
+        r = ctypes.c_int()
+        self._check(nat.lib().spst_backward_resolve(self._h, ctypes.byref(r)), "spst_backward_resolve")
+        return bool(r.value)
+
+    def forward_redone(self) -> bool:
+        """True if the last finalize re-ran the forward (work launched behind it is stale)."""
+        return bool(nat.lib().spst_forward_redone(self._h))
 
     def content_target(self):
         """(device uint8 copy of the bound window's content target, its scale)."""

@@ -76,22 +76,24 @@ class _Vec:
                                           nat.ptr(self.out), self._s()), None, "spst_vec_dots")
         return self.out[:len(pairs)].tolist()
 
-    def absmax(self, a):
+    def absmax(self, a, slot=0, read=True):
         nat.check(nat.lib().spst_vec_absmax(self.f64, nat.ptr(a), a.numel(), nat.ptr(self.partial),
-                                            nat.ptr(self.out), self._s()), None, "spst_vec_absmax")
-        return float(self.out[0].item())
+                                            nat.ptr(self.out[slot:]), self._s()), None, "spst_vec_absmax")
+        return float(self.out[slot].item()) if read else None
 
     def axpy(self, x, d, t, out):
         nat.check(nat.lib().spst_vec_axpy(self.f64, nat.ptr(x), nat.ptr(d), float(t), x.numel(), nat.ptr(out),
                                           self._s()), None, "spst_vec_axpy")
         return out
 
-    def sy(self, xt, x, gt, g, s, y):
+    def sy(self, xt, x, gt, g, s, y, read=True):
         nat.check(nat.lib().spst_vec_sy(self.f64, nat.ptr(xt), nat.ptr(x), nat.ptr(gt), nat.ptr(g), x.numel(),
                                         nat.ptr(s), nat.ptr(y), nat.ptr(self.partial), nat.ptr(self.out),
                                         self._s()), None, "spst_vec_sy")
-        ys, ss, yy = self.out[:3].tolist()
-        return ys, ss, yy
+        if read:
+            ys, ss, yy = self.out[:3].tolist()
+            return ys, ss, yy
+        return None
 
     # two-loop step primitives (device scalars)
     def axpy_dot(self, q_in, q_out, v, coef, cscale, w):
@@ -361,13 +363,27 @@ def minimize(f, x0, cfg: LBFGSConfig, callback=None, allreduce=None, resume: LBF
                 accepted = True
                 break
             t *= cfg.shrink
+        gmax_new = None
         if accepted:
-            if lazy:
-                g_try = obj.grad(g_spare)
-                trace.grads += 1
             spare = next(k for k in range(m + 1) if k not in slot_of)
             s, y = ring_s[spare], ring_y[spare]
-            ys, ss, yy = vec.sy(x_try, x, g_try, g, s, y)
+            if lazy and allreduce is None and hasattr(obj, "grad_resolve"):
+                # one host synchronisation for the gradient's range check, the curvature dots
+                # and max|g|: launch all three, then settle the backward (re-launching the
+                # vector passes in the rare case it had to be recomputed)
+                g_try = obj.grad(g_spare, defer=True)
+                trace.grads += 1
+                vec.sy(x_try, x, g_try, g, s, y, read=False)
+                vec.absmax(g_try, slot=3, read=False)
+                if obj.grad_resolve():
+                    vec.sy(x_try, x, g_try, g, s, y, read=False)
+                    vec.absmax(g_try, slot=3, read=False)
+                ys, ss, yy, gmax_new = vec.out[:4].tolist()
+            else:
+                if lazy:
+                    g_try = obj.grad(g_spare)
+                    trace.grads += 1
+                ys, ss, yy = vec.sy(x_try, x, g_try, g, s, y)
             if allreduce is not None:
                 tt = torch.tensor([ys, ss, yy], dtype=torch.float64, device=x.device)
                 allreduce(tt)
@@ -388,7 +404,7 @@ def minimize(f, x0, cfg: LBFGSConfig, callback=None, allreduce=None, resume: LBF
             if slot_of:
                 slot_of.pop(0)
         state.iter = it + 1
-        gmax = red_max(g)
+        gmax = gmax_new if gmax_new is not None else red_max(g)
         trace.losses.append(loss)
         trace.grad_norms.append(gmax)
         # callbacks and snapshots get their own copies (the reference hands out a fresh array

@@ -356,6 +356,8 @@ class Evaluation:
             counts = [eng.owned_pixels(i) for i in range(len(eng.style_taps))]
             content = eng.content_sqdiff() if p.has_content else None  # read after finalize's one sync
             terms, degenerate = eng.finalize(counts)
+            if content is not None and eng.forward_redone():  # the forward was re-run in careful mode
+                content = eng.content_sqdiff()
             _warn_degenerate(degenerate)
             total = float(terms.sum())
             if content is not None:
@@ -395,11 +397,13 @@ class Evaluation:
             ds.copy_(sv)
         return eng.finalize(_tap_counts(p.extractor, p.grid.image_h, p.grid.image_w, eng.style_taps))
 
-    def grad(self, out: torch.Tensor) -> torch.Tensor:
+    def grad(self, out: torch.Tensor, defer: bool = False) -> torch.Tensor:
+        """Gradient of the last ``loss`` point into ``out``.  defer=True (whole-image problems):
+        launch only; ``grad_resolve`` settles the backward's range check."""
         p, eng = self.p, self.p.engine
         two_lambda = 2.0 * p.weights.lambda_c if p.has_content else 0.0
         if self.whole:
-            eng.backward(two_lambda, out)
+            eng.backward(two_lambda, out, defer=defer)
             return out
         # windowed: pass 2 (reference localized.py:246-278)
         x_dev = self._x
@@ -412,6 +416,10 @@ class Evaluation:
                 eng.set_content_target(p.content_store.targets[wi])
             eng.backward(two_lambda, out)
         return out
+
+    def grad_resolve(self) -> bool:
+        """Settle a deferred gradient; True if it was rewritten (work launched on it is stale)."""
+        return self.p.engine.backward_resolve() if self.whole else False
 
 
 def loss_grad(x, p: TransferProblem):

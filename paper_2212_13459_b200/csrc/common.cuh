@@ -66,8 +66,6 @@ struct ConvArgs {
   int pool_max;
   uint32_t* pool_arg;
   int drain;                     // K-chunks per TMEM accumulation group (1 or 2)
-  int ksplit;                    // K-splits per tile (1: none; > 1: partials to split_ws, N = 128 only)
-  float* split_ws;               // [ksplit][tile][2 rows][N][128 px] fp32
   float comp[4];                 // round-toward-zero bias factor per group relative to `fine`:
                                  // [conv 1, conv 2, extra 1, extra 2 chunks]
   float fine;                    // common relative correction applied once to the drained sum

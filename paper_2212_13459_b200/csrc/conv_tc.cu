@@ -35,6 +35,12 @@ namespace spst {
 // RES ("resident weights", 64-channel GEMMs whose conv slab fits): the whole weight slab is
 // loaded once per CTA behind two activation-only stages, instead of re-streaming 37 KB per
 // chunk per tile -- those layers were bound by their operand loads.
+// Epilogue warps of the N=64 kernels.  16 (four warpgroups of 16 channels) was measured and
+// rejected: conv1_1 7.56 vs 4.95 ms, conv1_2 9.28 vs 8.86 ms (16-bit mask halves, more
+// partial-warp work) -- those layers are bound by their A-window stages, not by epilogue issue.
+#ifndef SPST_N64_EPIW
+#define SPST_N64_EPIW 8
+#endif
 template <int N, bool RES = false>
 struct ConvCfg {
   static constexpr int MT = 2;                      // output rows per tile (M = MT x 128 px)
@@ -61,9 +67,13 @@ struct ConvCfg {
   static constexpr int RES_OFF = STAGES * STAGE;     // resident slab (RES only)
   static constexpr int RES_MAX = RES ? 147456 : 0;   // up to 4 chunks of N=64 (C_in <= 64)
   static constexpr int NBUF = 512 / (MT * N);       // TMEM chunk buffers (MT rows x N each)
+  // epilogue warps: 8 = two warpgroups, one channel half each (SPST_N64_EPIW for N=64)
+  static constexpr int EPIW = N == 64 ? SPST_N64_EPIW : 8;
+  static constexpr int THREADS = 64 + 32 * EPIW;
   static constexpr int TMEM_COLS = 512;
   static constexpr int SMEM = STAGES * STAGE + RES_MAX + 1024;
-  static constexpr int CPG = MT == 2 ? N / 2 : N;   // channels per epilogue warpgroup
+  static constexpr int CPG = MT == 2 ? N / (EPIW / 4) : N;  // channels per epilogue warpgroup
+  static constexpr int NCH = CPG < 32 ? CPG : 32;   // channels per epilogue_ch call
   static constexpr int XB_OFF = (RES || 2 * XA_HALF > A_BYTES) ? 2 * XA_HALF : A_BYTES;  // extra-K slab offset
   static_assert(XB_OFF + XB_BYTES <= STAGE, "extra-K operand and slab must fit one stage");
   static_assert(SMEM + 2048 <= 232448, "dynamic + static shared memory must fit 227 KB");
@@ -164,6 +174,27 @@ __device__ __forceinline__ float warp_transpose_sum(float (&v)[32]) {
   return v[0];
 }
 
+// lane l < NCH gets the sum over the warp's 32 lanes of column l (NCH = 32: warp_transpose_sum;
+// NCH = 16: the same butterfly from offset 8, then the two half-warps are added)
+template <int NCH>
+__device__ __forceinline__ float warp_transpose_sum_n(float (&v)[NCH]) {
+  if constexpr (NCH == 32) {
+    return warp_transpose_sum(v);
+  } else {
+    const uint32_t lane = lane_id();
+#pragma unroll
+    for (int off = NCH / 2; off >= 1; off >>= 1) {
+#pragma unroll
+      for (int i = 0; i < off; ++i) {
+        float send = (lane & off) ? v[i] : v[i + off];
+        float keep = (lane & off) ? v[i + off] : v[i];
+        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+      }
+    }
+    return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 16);
+  }
+}
+
 __device__ __forceinline__ float warp_max(float v) {
 #pragma unroll
   for (int off = 16; off >= 1; off >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, off));
@@ -178,15 +209,18 @@ __device__ __forceinline__ void tmem_add32(uint32_t taddr, float* acc, float sca
   for (int i = 0; i < 32; ++i) acc[i] = fmaf(v[i], scale, acc[i]);
 }
 
-// Fused pointwise epilogue for 32 channels of one pixel in both rows (v0: row y0, v1: y0+1).
-template <int N>
-__device__ __forceinline__ void epilogue32(const ConvArgs& a, float* v0, float* v1, int ch0, int x, int y0,
-                                           int tile_xy, uint32_t q, float& amax0, float& amax1) {
+// Fused pointwise epilogue for NCH (32, or 16 with 16 epilogue warps) channels of one pixel in
+// both rows (v0: row y0, v1: y0+1).  ch0 is a multiple of NCH.
+template <int N, int NCH>
+__device__ __forceinline__ void epilogue_ch(const ConvArgs& a, float* v0, float* v1, int ch0, int x, int y0,
+                                            int tile_xy, uint32_t q, float& amax0, float& amax1) {
+  static_assert(NCH == 16 || NCH == 32, "16 or 32 channels per call");
   const uint32_t lane = lane_id();
+  constexpr int KG = NCH / 8;
   if (a.epi == EPI_FWD || a.epi == EPI_FWD_POOL) {
     uint32_t bits0 = 0, bits1 = 0;
 #pragma unroll
-    for (int j = 0; j < 32; ++j) {
+    for (int j = 0; j < NCH; ++j) {
       const float bj = a.bias ? __ldg(a.bias + ch0 + j) : 0.f;
       const float p0 = fmaf(v0[j], a.acc_scale, bj);
       const float p1 = fmaf(v1[j], a.acc_scale, bj);
@@ -197,27 +231,35 @@ __device__ __forceinline__ void epilogue32(const ConvArgs& a, float* v0, float* 
     }
     const bool ok0 = x < a.W && y0 < a.H, ok1 = x < a.W && y0 + 1 < a.H;
     if (a.mask_out) {
-      if (ok0) a.mask_out[((size_t)(ch0 >> 5) * a.H + y0) * a.W + x] = bits0;
-      if (ok1) a.mask_out[((size_t)(ch0 >> 5) * a.H + y0 + 1) * a.W + x] = bits1;
+      const size_t w0 = ((size_t)(ch0 >> 5) * a.H + y0) * a.W + x, w1 = w0 + a.W;
+      if constexpr (NCH == 32) {
+        if (ok0) a.mask_out[w0] = bits0;
+        if (ok1) a.mask_out[w1] = bits1;
+      } else {  // a 16-channel half of the 32-bit mask word (little endian)
+        uint16_t* m16 = reinterpret_cast<uint16_t*>(a.mask_out);
+        const int h = (ch0 >> 4) & 1;
+        if (ok0) m16[2 * w0 + h] = (uint16_t)bits0;
+        if (ok1) m16[2 * w1 + h] = (uint16_t)bits1;
+      }
     }
     if (a.epi == EPI_FWD || a.store_full) {
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
+      for (int k = 0; k < KG; ++k) {
         if (ok0) store_hl8<N == 64>(a.out, (ch0 >> 3) + k, y0, x, v0 + 8 * k, a.out.scale);
         if (ok1) store_hl8<N == 64>(a.out, (ch0 >> 3) + k, y0 + 1, x, v1 + 8 * k, a.out.scale);
       }
       if constexpr (N == 64) {  // (the N=128 kernel's codegen prefers the select form)
         if (ok0) {
 #pragma unroll
-          for (int j = 0; j < 32; ++j) amax0 = fmaxf(amax0, v0[j]);
+          for (int j = 0; j < NCH; ++j) amax0 = fmaxf(amax0, v0[j]);
         }
         if (ok1) {
 #pragma unroll
-          for (int j = 0; j < 32; ++j) amax0 = fmaxf(amax0, v1[j]);
+          for (int j = 0; j < NCH; ++j) amax0 = fmaxf(amax0, v1[j]);
         }
       } else {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
+        for (int j = 0; j < NCH; ++j) {
           amax0 = fmaxf(amax0, ok0 ? v0[j] : 0.f);
           amax0 = fmaxf(amax0, ok1 ? v1[j] : 0.f);
         }
@@ -227,21 +269,21 @@ __device__ __forceinline__ void epilogue32(const ConvArgs& a, float* v0, float* 
       const bool inx = x >= a.sum_c0 && x < a.sum_c1;
       const bool in0 = ok0 && inx && y0 >= a.sum_r0 && y0 < a.sum_r1;
       const bool in1 = ok1 && inx && y0 + 1 >= a.sum_r0 && y0 + 1 < a.sum_r1;
-      float s[32];
+      float s[NCH];
 #pragma unroll
-      for (int j = 0; j < 32; ++j) s[j] = (in0 ? v0[j] : 0.f) + (in1 ? v1[j] : 0.f);
-      const float tot = warp_transpose_sum(s);
-      a.colsum_partial[((size_t)tile_xy * 4 + q) * (size_t)(a.n_ntiles * N) + ch0 + lane] = tot;
+      for (int j = 0; j < NCH; ++j) s[j] = (in0 ? v0[j] : 0.f) + (in1 ? v1[j] : 0.f);
+      const float tot = warp_transpose_sum_n<NCH>(s);
+      if (lane < NCH) a.colsum_partial[((size_t)tile_xy * 4 + q) * (size_t)(a.n_ntiles * N) + ch0 + lane] = tot;
     }
     if (a.epi == EPI_FWD_POOL) {
-      float pv[32];
+      float pv[NCH];
       const int px = x >> 1, py = y0 >> 1;
       if (a.pool_max) {
         // first-argmax over the window in row-major order (x, y0), (x+1, y0), (x, y0+1),
         // (x+1, y0+1): strict '>' keeps the first of equal values (np.argmax)
         uint32_t arg0 = 0, arg1 = 0;
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
+        for (int j = 0; j < NCH; ++j) {
           const float b = __shfl_xor_sync(0xffffffffu, v0[j], 1), d = __shfl_xor_sync(0xffffffffu, v1[j], 1);
           float m = v0[j];
           uint32_t idx = 0;
@@ -255,20 +297,20 @@ __device__ __forceinline__ void epilogue32(const ConvArgs& a, float* v0, float* 
         if ((lane & 1) == 0 && px < a.out_pool.W && py < a.out_pool.H) {
           const size_t plane = (size_t)a.out_pool.H * a.out_pool.W, o = (size_t)py * a.out_pool.W + px;
           a.pool_arg[(size_t)(ch0 >> 4) * plane + o] = arg0;
-          a.pool_arg[(size_t)((ch0 >> 4) + 1) * plane + o] = arg1;
+          if constexpr (NCH == 32) a.pool_arg[(size_t)((ch0 >> 4) + 1) * plane + o] = arg1;
         }
       } else {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
+        for (int j = 0; j < NCH; ++j) {
           const float s2 = v0[j] + v1[j];
           pv[j] = (s2 + __shfl_xor_sync(0xffffffffu, s2, 1)) * 0.25f;
         }
       }
       if ((lane & 1) == 0 && px < a.out_pool.W && py < a.out_pool.H) {
 #pragma unroll
-        for (int k = 0; k < 4; ++k) store_hl8<N == 64>(a.out_pool, (ch0 >> 3) + k, py, px, pv + 8 * k, a.out_pool.scale);
+        for (int k = 0; k < KG; ++k) store_hl8<N == 64>(a.out_pool, (ch0 >> 3) + k, py, px, pv + 8 * k, a.out_pool.scale);
 #pragma unroll
-        for (int j = 0; j < 32; ++j) amax1 = fmaxf(amax1, pv[j]);
+        for (int j = 0; j < NCH; ++j) amax1 = fmaxf(amax1, pv[j]);
       }
     }
   } else if (a.epi == EPI_BWD) {
@@ -278,10 +320,10 @@ __device__ __forceinline__ void epilogue32(const ConvArgs& a, float* v0, float* 
       const int y = y0 + r;
       if (x >= a.W || y >= a.H) continue;
 #pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] = fmaf(v[j], a.acc_scale, a.bias ? __ldg(a.bias + ch0 + j) : 0.f);
+      for (int j = 0; j < NCH; ++j) v[j] = fmaf(v[j], a.acc_scale, a.bias ? __ldg(a.bias + ch0 + j) : 0.f);
       if (a.content_coef != 0.f) {
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < KG; ++k) {
           float cv[8], cu[8];
           load_hl8(a.content_v, (ch0 >> 3) + k, y, x, cv);
           load_hl8(a.content_u, (ch0 >> 3) + k, y, x, cu);
@@ -291,7 +333,7 @@ __device__ __forceinline__ void epilogue32(const ConvArgs& a, float* v0, float* 
       }
       if (a.addend.hi) {
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < KG; ++k) {
           float ad[8];
           load_hl8(a.addend, (ch0 >> 3) + k, y, x, ad);
 #pragma unroll
@@ -299,14 +341,14 @@ __device__ __forceinline__ void epilogue32(const ConvArgs& a, float* v0, float* 
         }
       }
       if (a.mask_in) {
-        const uint32_t bits = a.mask_in[((size_t)(ch0 >> 5) * a.H + y) * a.W + x];
+        const uint32_t bits = a.mask_in[((size_t)(ch0 >> 5) * a.H + y) * a.W + x] >> (ch0 & 16);
 #pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = ((bits >> j) & 1u) ? v[j] : 0.f;
+        for (int j = 0; j < NCH; ++j) v[j] = ((bits >> j) & 1u) ? v[j] : 0.f;
       }
 #pragma unroll
-      for (int j = 0; j < 32; ++j) amax0 = fmaxf(amax0, fabsf(v[j]));
+      for (int j = 0; j < NCH; ++j) amax0 = fmaxf(amax0, fabsf(v[j]));
 #pragma unroll
-      for (int k = 0; k < 4; ++k) store_hl8<N == 64>(a.out, (ch0 >> 3) + k, y, x, v + 8 * k, a.out.scale);
+      for (int k = 0; k < KG; ++k) store_hl8<N == 64>(a.out, (ch0 >> 3) + k, y, x, v + 8 * k, a.out.scale);
     }
   } else {  // EPI_BWD_POOL: out is the 2x finer grid
 #pragma unroll
@@ -320,31 +362,31 @@ __device__ __forceinline__ void epilogue32(const ConvArgs& a, float* v0, float* 
       if (a.pool_max) {
         const size_t plane = (size_t)a.H * a.W, o = (size_t)y * a.W + x;
         arg0 = a.pool_arg[(size_t)(ch0 >> 4) * plane + o];
-        arg1 = a.pool_arg[(size_t)((ch0 >> 4) + 1) * plane + o];
+        if constexpr (NCH == 32) arg1 = a.pool_arg[(size_t)((ch0 >> 4) + 1) * plane + o];
       }
       const float sc = a.pool_max ? a.acc_scale : a.acc_scale * 0.25f;
 #pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] *= sc;
+      for (int j = 0; j < NCH; ++j) v[j] *= sc;
 #pragma unroll
       for (int i = 0; i < 2; ++i)
 #pragma unroll
         for (int jx = 0; jx < 2; ++jx) {
           const int yy = 2 * y + i, xx = 2 * x + jx;
-          float w[32];
+          float w[NCH];
           if (a.pool_max) {
             const uint32_t want = 2 * i + jx;
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
+            for (int j = 0; j < NCH; ++j) {
               const uint32_t idx = ((j < 16 ? arg0 : arg1) >> (2 * (j & 15))) & 3u;
               w[j] = idx == want ? v[j] : 0.f;
             }
           } else {
 #pragma unroll
-            for (int j = 0; j < 32; ++j) w[j] = v[j];
+            for (int j = 0; j < NCH; ++j) w[j] = v[j];
           }
           if (a.addend.hi) {
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
+            for (int k = 0; k < KG; ++k) {
               float ad[8];
               load_hl8(a.addend, (ch0 >> 3) + k, yy, xx, ad);
 #pragma unroll
@@ -352,14 +394,14 @@ __device__ __forceinline__ void epilogue32(const ConvArgs& a, float* v0, float* 
             }
           }
           if (a.mask_in) {
-            const uint32_t bits = a.mask_in[((size_t)(ch0 >> 5) * a.out.H + yy) * a.out.W + xx];
+            const uint32_t bits = a.mask_in[((size_t)(ch0 >> 5) * a.out.H + yy) * a.out.W + xx] >> (ch0 & 16);
 #pragma unroll
-            for (int j = 0; j < 32; ++j) w[j] = ((bits >> j) & 1u) ? w[j] : 0.f;
+            for (int j = 0; j < NCH; ++j) w[j] = ((bits >> j) & 1u) ? w[j] : 0.f;
           }
 #pragma unroll
-          for (int j = 0; j < 32; ++j) amax0 = fmaxf(amax0, fabsf(w[j]));
+          for (int j = 0; j < NCH; ++j) amax0 = fmaxf(amax0, fabsf(w[j]));
 #pragma unroll
-          for (int k = 0; k < 4; ++k) store_hl8<N == 64>(a.out, (ch0 >> 3) + k, yy, xx, w + 8 * k, a.out.scale);
+          for (int k = 0; k < KG; ++k) store_hl8<N == 64>(a.out, (ch0 >> 3) + k, yy, xx, w + 8 * k, a.out.scale);
         }
     }
   }
@@ -382,7 +424,7 @@ __device__ __forceinline__ TileId decode_tile(const ConvArgs& a, int t) {
 }
 
 template <int N, bool RES>
-__global__ void __launch_bounds__(320, 1) conv3x3_tc_kernel(const __grid_constant__ ConvArgs a) {
+__global__ void __launch_bounds__(ConvCfg<N, RES>::THREADS, 1) conv3x3_tc_kernel(const __grid_constant__ ConvArgs a) {
   using C = ConvCfg<N, RES>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -396,11 +438,6 @@ __global__ void __launch_bounds__(320, 1) conv3x3_tc_kernel(const __grid_constan
   const int first = (int)blockIdx.x;
   const int step = (int)gridDim.x;
   const int n_chunks = a.n_kc + a.n_xkc;
-  // work unit u = (tile u / S, K-split u % S): split j covers chunks [j C / S, (j+1) C / S)
-  // (S = a.ksplit > 1 only for grids under ~2.5 waves; the partials are summed in split order
-  // by split_finish_kernel, which runs the epilogue)
-  const int S = a.ksplit;
-  const int n_units = n_tiles * S;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&a.tm_r_hi);
@@ -413,7 +450,7 @@ __global__ void __launch_bounds__(320, 1) conv3x3_tc_kernel(const __grid_constan
     }
     for (int b = 0; b < C::NBUF; ++b) {
       mbar_init(&cfull_bar[b], 1);
-      mbar_init(&cempty_bar[b], 8);
+      mbar_init(&cempty_bar[b], C::EPIW);
     }
     mbar_init(&res_bar, 1);
     fence_barrier_init();
@@ -441,13 +478,12 @@ __global__ void __launch_bounds__(320, 1) conv3x3_tc_kernel(const __grid_constan
       }
     }
     uint32_t g = 0;
-    for (int u = first; u < n_units; u += step) {
-      const int t = u / S, j = u - t * S;
+    for (int t = first; t < n_tiles; t += step) {
       const TileId id = decode_tile(a, t);
       const int nt = id.nt;
       const int x0 = id.cx * 128;
       const int y0 = id.ry * C::MT;
-      for (int c = j * n_chunks / S; c < (j + 1) * n_chunks / S; ++c, ++g) {
+      for (int c = 0; c < n_chunks; ++c, ++g) {
         const int s = g % C::STAGES;
         mbar_wait(&empty_bar[s], ((g / C::STAGES) & 1) ^ 1);
         uint8_t* st = smem + s * C::STAGE;
@@ -479,9 +515,8 @@ __global__ void __launch_bounds__(320, 1) conv3x3_tc_kernel(const __grid_constan
       const uint32_t idesc = make_idesc_f16(128, N, 0, 0, 0);
       if constexpr (RES) mbar_wait(&res_bar, 0);
       uint32_t g = 0, gq = 0;  // chunk counter (smem stages), group counter (TMEM buffers)
-      for (int u = first; u < n_units; u += step) {
-        const int j = u % S;
-        for (int c = j * n_chunks / S; c < (j + 1) * n_chunks / S; ++c, ++g) {
+      for (int t = first; t < n_tiles; t += step) {
+        for (int c = 0; c < n_chunks; ++c, ++g) {
           bool gfirst, glast;
           chunk_group(a.drain, c, a.n_kc, n_chunks, gfirst, glast);
           const uint32_t b = gq % C::NBUF;
@@ -576,8 +611,7 @@ __global__ void __launch_bounds__(320, 1) conv3x3_tc_kernel(const __grid_constan
     const int rp = C::MT == 2 ? 0 : (int)grp;            // row pair handled by this warpgroup
     const int cofs = C::MT == 2 ? (int)grp * C::CPG : 0;  // first channel handled
     uint32_t g = 0;
-    for (int u = first; u < n_units; u += step) {
-      const int t = u / S, j = u - t * S;
+    for (int t = first; t < n_tiles; t += step) {
       const TileId id = decode_tile(a, t);
       const int nt = id.nt, cx = id.cx, ry = id.ry;
       const int x0 = cx * 128, y0 = ry * C::MT + 2 * rp;
@@ -586,10 +620,9 @@ __global__ void __launch_bounds__(320, 1) conv3x3_tc_kernel(const __grid_constan
 #pragma unroll
       for (int i = 0; i < C::CPG; ++i) acc0[i] = acc1[i] = 0.f;
       const int D = a.drain;
-      // accumulation groups of the unit's chunk range, as the MMA issuer forms them (chunk_group):
-      // up to D chunks of one kind
-      const int ce = (j + 1) * n_chunks / S;
-      for (int c = j * n_chunks / S; c < ce; ++g) {
+      // accumulation groups as the MMA issuer forms them (chunk_group): up to D chunks of one kind
+      const int ce = n_chunks;
+      for (int c = 0; c < ce; ++g) {
         const bool xg = c >= a.n_kc;
         const int gsz = min(D, (xg ? ce : min(ce, a.n_kc)) - c);
         c += gsz;
@@ -605,6 +638,14 @@ __global__ void __launch_bounds__(320, 1) conv3x3_tc_kernel(const __grid_constan
           tmem_ld32x2(trow, trow + N, v0, v1);
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
+            acc0[i] = fmaf(v0[i], cs, acc0[i]);
+            acc1[i] = fmaf(v1[i], cs, acc1[i]);
+          }
+        } else if constexpr (C::CPG == 16) {
+          float v0[16], v1[16];
+          tmem_ld16x2(trow, trow + N, v0, v1);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
             acc0[i] = fmaf(v0[i], cs, acc0[i]);
             acc1[i] = fmaf(v1[i], cs, acc1[i]);
           }
@@ -626,23 +667,12 @@ __global__ void __launch_bounds__(320, 1) conv3x3_tc_kernel(const __grid_constan
         acc0[i] = fmaf(acc0[i], a.fine, acc0[i]);
         acc1[i] = fmaf(acc1[i], a.fine, acc1[i]);
       }
-      if constexpr (N == 128 && C::MT == 2) {
-        if (S > 1) {  // K-split partial -> workspace [split][tile][row][channel][px] (coalesced in px)
-          float* w = a.split_ws + ((size_t)(j * n_tiles + t) * 2) * N * 128;
-#pragma unroll
-          for (int i = 0; i < C::CPG; ++i) {
-            w[(size_t)(cofs + i) * 128 + m] = acc0[i];
-            w[(size_t)(N + cofs + i) * 128 + m] = acc1[i];
-          }
-          continue;
-        }
-      }
       float amax0 = 0.f, amax1 = 0.f;
       const int part_row = (ry * a.tiles_x + cx) * (C::MT / 2) + rp;
 #pragma unroll
-      for (int cb = 0; cb < C::CPG / 32; ++cb)
-        epilogue32<N>(a, acc0 + cb * 32, acc1 + cb * 32, nt * N + cofs + cb * 32, x, y0, part_row, q, amax0,
-                      amax1);
+      for (int cb = 0; cb < C::CPG / C::NCH; ++cb)
+        epilogue_ch<N, C::NCH>(a, acc0 + cb * C::NCH, acc1 + cb * C::NCH, nt * N + cofs + cb * C::NCH, x, y0,
+                               part_row, q, amax0, amax1);
       if (a.amax) {
         amax0 = warp_max(amax0);
         amax1 = warp_max(amax1);
@@ -658,47 +688,6 @@ __global__ void __launch_bounds__(320, 1) conv3x3_tc_kernel(const __grid_constan
   if (warp == 1) tmem_dealloc<C::TMEM_COLS>(tmem_base);
 }
 
-// K-split finish (N = 128): one CTA per tile with the conv epilogue's thread mapping (8 warps:
-// TMEM quarter q = pixels 32q..32q+31, warpgroup = channel half); sums the S partials in split
-// order (deterministic) and runs the same fused epilogue.
-__global__ void __launch_bounds__(256) split_finish_kernel(const __grid_constant__ ConvArgs a) {
-  using C = ConvCfg<128, false>;
-  constexpr int N = 128;
-  const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
-  const uint32_t q = warp & 3, grp = warp >> 2;
-  const int m = q * 32 + lane;
-  const int cofs = (int)grp * C::CPG;
-  const int n_tiles = a.tiles_x * a.tiles_y * a.n_ntiles;
-  const int t = blockIdx.x;
-  const TileId id = decode_tile(a, t);
-  const int x = id.cx * 128 + m, y0 = id.ry * C::MT;
-  const int part_row = (id.ry * a.tiles_x + id.cx) * (C::MT / 2);
-  float amax0 = 0.f, amax1 = 0.f;
-#pragma unroll
-  for (int cb = 0; cb < C::CPG / 32; ++cb) {
-    float v0[32], v1[32];
-#pragma unroll
-    for (int i = 0; i < 32; ++i) v0[i] = v1[i] = 0.f;
-    for (int j = 0; j < a.ksplit; ++j) {
-      const float* w = a.split_ws + ((size_t)(j * n_tiles + t) * 2) * N * 128;
-#pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        v0[i] += w[(size_t)(cofs + cb * 32 + i) * 128 + m];
-        v1[i] += w[(size_t)(N + cofs + cb * 32 + i) * 128 + m];
-      }
-    }
-    epilogue32<N>(a, v0, v1, id.nt * N + cofs + cb * 32, x, y0, part_row, q, amax0, amax1);
-  }
-  if (a.amax) {
-    amax0 = warp_max(amax0);
-    amax1 = warp_max(amax1);
-    if (lane == 0) {
-      if (amax0 > 0.f) atomicMax(a.amax, __float_as_uint(amax0));
-      if (amax1 > 0.f) atomicMax(a.amax + 1, __float_as_uint(amax1));
-    }
-  }
-}
-
 // ------------------------------------------------------------------------------------------
 int conv_tc_smem_bytes(int N) { return N == 128 ? ConvCfg<128>::SMEM : ConvCfg<64>::SMEM; }
 int conv_tc_rows(int N) { return N == 128 ? ConvCfg<128>::MT : ConvCfg<64>::MT; }
@@ -708,7 +697,7 @@ template <int N, bool RES>
 static cudaError_t launch_one(const ConvArgs& a, int grid, cudaStream_t stream) {
   auto k = conv3x3_tc_kernel<N, RES>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, ConvCfg<N, RES>::SMEM);
-  note_launch(), k<<<grid, 320, ConvCfg<N, RES>::SMEM, stream>>>(a);
+  note_launch(), k<<<grid, ConvCfg<N, RES>::THREADS, ConvCfg<N, RES>::SMEM, stream>>>(a);
   return cudaGetLastError();
 }
 
@@ -718,12 +707,7 @@ bool conv_tc_resident_ok(int N, int n_ntiles, int n_kc) {
 }
 
 cudaError_t launch_conv_tc(const ConvArgs& a, int N, int grid, cudaStream_t stream) {
-  if (N == 128) {
-    cudaError_t e = launch_one<128, false>(a, grid, stream);
-    if (e != cudaSuccess || a.ksplit <= 1) return e;
-    note_launch(), split_finish_kernel<<<a.tiles_x * a.tiles_y * a.n_ntiles, 256, 0, stream>>>(a);
-    return cudaGetLastError();
-  }
+  if (N == 128) return launch_one<128, false>(a, grid, stream);
   return conv_tc_resident_ok(N, a.n_ntiles, a.n_kc) ? launch_one<64, true>(a, grid, stream)
                                                     : launch_one<64, false>(a, grid, stream);
 }

@@ -135,24 +135,6 @@ int bwd_drain() {
   return d;
 }
 
-// K-splits for a conv launch of `tiles` (2-row x 128-px x N) tiles of `chunks` K-chunks: a
-// persistent grid of 148 CTAs finishes in ceil(units / 148) rounds of ceil(chunks / S) chunks;
-// splitting pays when the tiles fill under ~2.5 waves (the deep layers of coarse scales and
-// per-rank windows).  The finish kernel costs ~3 chunk times.  SPST_KSPLIT=1 disables.
-int choose_ksplit(int tiles, int chunks) {
-  static const int cap = std::max(1, std::min(8, env_int("SPST_KSPLIT", 8)));
-  double best = std::ceil(tiles / (double)kSMs) * chunks;
-  int best_s = 1;
-  for (int S = 2; S <= cap && chunks / S >= 2; ++S) {
-    const double cost = std::ceil(tiles * (double)S / kSMs) * std::ceil(chunks / (double)S) + 3.0;
-    if (cost < 0.93 * best) {
-      best = cost;
-      best_s = S;
-    }
-  }
-  return best_s;
-}
-
 // comp[] / fine of a conv launch (conv_tc.cu): a conv chunk is 18 correction MMAs then 9 hi*hi
 // MMAs per output row; an extra-K chunk xkg correction then xkg/2 hi*hi MMAs.  `fine` carries
 // the full conv group's correction; comp[] the difference of every other group composition.
@@ -295,8 +277,6 @@ struct spst_ctx {
   double bwd_lambda = 0.0;
   float* bwd_grad = nullptr;
   unsigned int* amax_pin = nullptr;  // [4 * stages + 4]
-  float* split_ws = nullptr;         // K-split partials (conv_tc.cu), grown on demand
-  size_t split_ws_bytes = 0;
   double* fin_pin = nullptr;
   size_t fin_count = 0;
 
@@ -628,28 +608,8 @@ int run_conv(spst_ctx* ctx, ConvLaunch& L) {
   a.drain = L.drain;
   if (a.n_kc + a.n_xkc == 0) return ctx->fail(SPST_ERR_CONFIG, "empty GEMM");
   const int tiles = a.tiles_x * a.tiles_y * a.n_ntiles;
-  a.ksplit = 1;
-  a.split_ws = nullptr;
-  if (N == 128 && a.n_kc > 0) {
-    a.ksplit = choose_ksplit(tiles, a.n_kc + a.n_xkc);
-    if (a.ksplit > 1) {
-      a.drain = 1;  // split units drain every chunk (a unit's range may start mid-group)
-      const size_t need = (size_t)a.ksplit * tiles * 2 * 128 * 128 * sizeof(float);
-      if (need > ctx->split_ws_bytes) {
-        if (ctx->split_ws) {
-          cudaStreamSynchronize(ctx->stream);
-          cudaFree(ctx->split_ws);
-        }
-        ctx->split_ws = nullptr;
-        ctx->split_ws_bytes = 0;
-        CK(cudaMalloc(&ctx->split_ws, need));
-        ctx->split_ws_bytes = need;
-      }
-      a.split_ws = ctx->split_ws;
-    }
-  }
   set_conv_comp(a, N);
-  const int grid = std::min(tiles * a.ksplit, kSMs);  // persistent: one CTA per SM
+  const int grid = std::min(tiles, kSMs);  // persistent: one CTA per SM
   auto* tm = timer_begin(ctx, N == 128 ? 0 : 1, L.flops);
   CK(launch_conv_tc(a, N, grid, ctx->stream));
   timer_end(ctx, tm);
@@ -1341,7 +1301,6 @@ void spst_destroy(spst_ctx* ctx) {
   if (ctx->bound) settle(ctx);
   ctx->release_bound();
   if (ctx->amax_pin) cudaFreeHost(ctx->amax_pin);
-  if (ctx->split_ws) cudaFree(ctx->split_ws);
   if (ctx->fin_pin) cudaFreeHost(ctx->fin_pin);
   if (ctx->pool) cudaMemPoolDestroy(ctx->pool);
   for (void* p : ctx->persistent) cudaFree(p);
@@ -1872,7 +1831,6 @@ int spst_debug_conv(int device, int mode, int cin, int cout, int H, int W, const
   }
   CK(cudaDeviceSynchronize());
   ctx->release_bound();
-  if (ctx->split_ws) cudaFree(ctx->split_ws);
   return SPST_OK;
 }
 

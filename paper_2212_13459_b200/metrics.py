@@ -90,17 +90,12 @@ def ssim(a, b) -> float:
 
 def gram_distance(x, v, spec, block: int = 512, margin: int = 256, weights: dict | None = None,
                   threads: int = 1) -> float:
-    """Sum over style taps of w_L * ||G(x) - G(v)||_F^2 using blockwise statistics.
-
-    weights maps tap name to w_L; None means 1 for every tap (the unweighted Gram metric).
-    """
-    sx = stats_pass(x, spec, block=block, margin=margin, threads=threads)
-    sv = stats_pass(v, spec, block=block, margin=margin, threads=threads)
-    total = 0.0
-    for t in spec.style_taps:
-        w = 1.0 if weights is None else weights[t]
-        total += w * float(np.sum((sx[t].gram - sv[t].gram) ** 2))
-    return total
+    """Weighted squared Frobenius distance between the Gram matrices of x and v, summed over
+    the style taps (reference metrics.py:76-89).  Both images go through the device
+    ``stats_pass`` on the given grid; ``weights`` ({tap: w}) defaults to 1 per tap."""
+    grams = [stats_pass(img, spec, block=block, margin=margin, threads=threads) for img in (x, v)]
+    return sum((1.0 if weights is None else weights[t]) * float(np.sum((grams[0][t].gram - grams[1][t].gram) ** 2))
+               for t in spec.style_taps)
 
 
 @dataclass(frozen=True)

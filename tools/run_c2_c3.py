@@ -6,8 +6,8 @@ C2: single scale, 1512x2016 content, 1024x1024 style, 100 L-BFGS iterations (his
     the reference's first scale, pipeline.py:32-33).  Before the run, one evaluation at a
     perturbed iterate is checked against the f64 oracle (oracle/spst_oracle.py, whole-image
     restatement of the reference's Algorithm 1 — test infrastructure, run here as the checker
-    only): loss within 1e-3 and the gradient on our ReLU pattern within 1e-4 are asserted; the
-    plain gradient difference is reported next to the oracle's own f32-vs-f64 difference.
+    only): loss within 1e-5, the gradient within the north-star bar max(1e-3, 1.5 x the
+    oracle's own f32-vs-f64 difference) and, on our ReLU pattern, within 5e-6 are asserted.
 C3: multiscale_transfer with 3 scales, 756x1008 -> 1512x2016 -> 3024x4032 content, style
     2113x2660, fast schedule; per-scale iterations and time.
 """
@@ -64,10 +64,11 @@ if not a.no_oracle:
     rl, rg, ra, r32 = abs(loss - lo) / abs(lo), rel(g, go), rel(g, gm), rel(g32, go)
     c2["oracle_f64"] = {"loss": lo, "loss_rel": rl, "grad_rel_l2": rg, "grad_rel_l2_on_our_masks": ra,
                         "oracle_f32_grad_rel_l2": r32, "seconds": time.time() - t0,
-                        "bounds": {"loss_rel": 1e-3, "grad_rel_l2_on_our_masks": 1e-4}}
+                        "bounds": {"loss_rel": 1e-5, "grad_rel_l2": max(1e-3, 1.5 * r32),
+                                   "grad_rel_l2_on_our_masks": 5e-6}}
     print(f"C2 vs f64 oracle: loss rel {rl:.2e}; grad rel-L2 {rg:.2e} (oracle's own f32 path {r32:.2e}); "
           f"on our ReLU masks {ra:.2e} ({time.time() - t0:.0f} s CPU)", flush=True)
-    assert rl <= 1e-3 and ra <= 1e-4, (rl, ra)
+    assert rl <= 1e-5 and ra <= 5e-6 and rg <= max(1e-3, 1.5 * r32), (rl, rg, ra, r32)
 obj = objective_for(p)
 x0 = torch.from_numpy(u).cuda()
 minimize(obj, x0, LBFGSConfig(history_size=100, max_iters=3))  # module load / first binds

@@ -10,12 +10,13 @@
 // GEMM view: M = output pixels (a CTA tile is 2 rows x 128 px = two M=128 accumulators),
 // N = output channels (64/128 per tile), K = 9 taps x input channels.
 //
-// Numerics ("fp16x3 + register accumulation"): operands are fp16 hi/lo pairs with
+// Numerics ("fp16x3 + compensated register accumulation"): operands are fp16 hi/lo pairs with
 // power-of-two tensor scales; each 16-channel K-chunk issues hi*lo + lo*hi + hi*hi over the 9
-// taps into a FRESH TMEM accumulator shared by at most D chunks (D = 2 on the 128-channel
-// layers, 1 on the 64-channel ones), and the epilogue warps drain it into fp32 registers
-// (round-to-nearest adds).  The tensor core therefore never carries a long running sum, which
-// removes the truncation bias of long in-TMEM accumulations (rel-err ~ K x 2^-24 otherwise).
+// taps into a FRESH TMEM accumulator shared by at most D chunks (ConvArgs::drain: 1 in the
+// forward, whose ReLU signs must be fp32-class, 2 in the backward), and the epilogue warps
+// drain it into fp32 registers (round-to-nearest adds), multiplying out the expected
+// round-toward-zero shrink of the tensor core's accumulation (comp[] / fine, see below and
+// DESIGN.md §5).  The tensor core never carries a long running sum.
 //
 // Warp roles (320 threads, persistent over output tiles, one CTA per SM):
 //   warp 0      TMA producer: per K-chunk the 4-row halo window of hi and lo activations as
@@ -211,9 +212,12 @@ __device__ __forceinline__ void tmem_add32(uint32_t taddr, float* acc, float sca
 
 // Fused pointwise epilogue for NCH (32, or 16 with 16 epilogue warps) channels of one pixel in
 // both rows (v0: row y0, v1: y0+1).  ch0 is a multiple of NCH.
+// mpre (nullable): the tile's ReLU mask words for these 32 channels, loaded at tile start (EPI_BWD:
+// [row]; EPI_BWD_POOL: [row * 4 + i * 2 + jx]); bpre (nullable): the channels' bias in registers.
 template <int N, int NCH>
 __device__ __forceinline__ void epilogue_ch(const ConvArgs& a, float* v0, float* v1, int ch0, int x, int y0,
-                                            int tile_xy, uint32_t q, float& amax0, float& amax1) {
+                                            int tile_xy, uint32_t q, float& amax0, float& amax1,
+                                            const uint32_t* mpre = nullptr, const float* bpre = nullptr) {
   static_assert(NCH == 16 || NCH == 32, "16 or 32 channels per call");
   const uint32_t lane = lane_id();
   constexpr int KG = NCH / 8;
@@ -221,7 +225,7 @@ __device__ __forceinline__ void epilogue_ch(const ConvArgs& a, float* v0, float*
     uint32_t bits0 = 0, bits1 = 0;
 #pragma unroll
     for (int j = 0; j < NCH; ++j) {
-      const float bj = a.bias ? __ldg(a.bias + ch0 + j) : 0.f;
+      const float bj = bpre ? bpre[j] : (a.bias ? __ldg(a.bias + ch0 + j) : 0.f);
       const float p0 = fmaf(v0[j], a.acc_scale, bj);
       const float p1 = fmaf(v1[j], a.acc_scale, bj);
       bits0 |= (p0 > 0.f ? 1u : 0u) << j;
@@ -320,7 +324,8 @@ __device__ __forceinline__ void epilogue_ch(const ConvArgs& a, float* v0, float*
       const int y = y0 + r;
       if (x >= a.W || y >= a.H) continue;
 #pragma unroll
-      for (int j = 0; j < NCH; ++j) v[j] = fmaf(v[j], a.acc_scale, a.bias ? __ldg(a.bias + ch0 + j) : 0.f);
+      for (int j = 0; j < NCH; ++j)
+        v[j] = fmaf(v[j], a.acc_scale, bpre ? bpre[j] : (a.bias ? __ldg(a.bias + ch0 + j) : 0.f));
       if (a.content_coef != 0.f) {
 #pragma unroll
         for (int k = 0; k < KG; ++k) {
@@ -341,7 +346,8 @@ __device__ __forceinline__ void epilogue_ch(const ConvArgs& a, float* v0, float*
         }
       }
       if (a.mask_in) {
-        const uint32_t bits = a.mask_in[((size_t)(ch0 >> 5) * a.H + y) * a.W + x] >> (ch0 & 16);
+        const uint32_t bits =
+            (mpre ? mpre[r] : a.mask_in[((size_t)(ch0 >> 5) * a.H + y) * a.W + x]) >> (ch0 & 16);
 #pragma unroll
         for (int j = 0; j < NCH; ++j) v[j] = ((bits >> j) & 1u) ? v[j] : 0.f;
       }
@@ -394,7 +400,9 @@ __device__ __forceinline__ void epilogue_ch(const ConvArgs& a, float* v0, float*
             }
           }
           if (a.mask_in) {
-            const uint32_t bits = a.mask_in[((size_t)(ch0 >> 5) * a.out.H + yy) * a.out.W + xx] >> (ch0 & 16);
+            const uint32_t bits =
+                (mpre ? mpre[r * 4 + i * 2 + jx] : a.mask_in[((size_t)(ch0 >> 5) * a.out.H + yy) * a.out.W + xx]) >>
+                (ch0 & 16);
 #pragma unroll
             for (int j = 0; j < NCH; ++j) w[j] = ((bits >> j) & 1u) ? w[j] : 0.f;
           }
@@ -611,11 +619,39 @@ __global__ void __launch_bounds__(ConvCfg<N, RES>::THREADS, 1) conv3x3_tc_kernel
     const int rp = C::MT == 2 ? 0 : (int)grp;            // row pair handled by this warpgroup
     const int cofs = C::MT == 2 ? (int)grp * C::CPG : 0;  // first channel handled
     uint32_t g = 0;
+    // max |output| over all of this thread's tiles: one atomic per warp per launch (a per-tile
+    // atomic on the same two words from every SM serialised in L2)
+    float amax0 = 0.f, amax1 = 0.f;
+    // N=64 (one epilogue_ch call per thread and tile): bias in registers for the whole launch,
+    // ReLU mask words fetched at tile start so their latency hides behind the drains
+    constexpr bool PRE = N == 64 && C::CPG == 32;
+    float bpre[PRE ? 32 : 1];
+    int bias_nt = -1;
     for (int t = first; t < n_tiles; t += step) {
       const TileId id = decode_tile(a, t);
       const int nt = id.nt, cx = id.cx, ry = id.ry;
       const int x0 = cx * 128, y0 = ry * C::MT + 2 * rp;
       const int x = x0 + m;
+      uint32_t mpre[PRE ? 8 : 1];
+      if constexpr (PRE) {
+        const int ch0 = nt * N + cofs;
+        if (nt != bias_nt) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) bpre[j] = a.bias ? __ldg(a.bias + ch0 + j) : 0.f;
+          bias_nt = nt;
+        }
+        if (a.mask_in && a.epi == EPI_BWD) {
+#pragma unroll
+          for (int r = 0; r < 2; ++r)
+            mpre[r] = (x < a.W && y0 + r < a.H) ? a.mask_in[((size_t)(ch0 >> 5) * a.H + y0 + r) * a.W + x] : 0u;
+        } else if (a.mask_in && a.epi == EPI_BWD_POOL) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const int r = k >> 2, yy = 2 * (y0 + r) + ((k >> 1) & 1), xx = 2 * x + (k & 1);
+            mpre[k] = (x < a.W && y0 + r < a.H) ? a.mask_in[((size_t)(ch0 >> 5) * a.out.H + yy) * a.out.W + xx] : 0u;
+          }
+        }
+      }
       float acc0[C::CPG], acc1[C::CPG];
 #pragma unroll
       for (int i = 0; i < C::CPG; ++i) acc0[i] = acc1[i] = 0.f;
@@ -667,19 +703,23 @@ __global__ void __launch_bounds__(ConvCfg<N, RES>::THREADS, 1) conv3x3_tc_kernel
         acc0[i] = fmaf(acc0[i], a.fine, acc0[i]);
         acc1[i] = fmaf(acc1[i], a.fine, acc1[i]);
       }
-      float amax0 = 0.f, amax1 = 0.f;
       const int part_row = (ry * a.tiles_x + cx) * (C::MT / 2) + rp;
+      if constexpr (PRE) {
+        epilogue_ch<N, 32>(a, acc0, acc1, nt * N + cofs, x, y0, part_row, q, amax0, amax1,
+                           a.mask_in ? mpre : nullptr, bpre);
+      } else {
 #pragma unroll
-      for (int cb = 0; cb < C::CPG / C::NCH; ++cb)
-        epilogue_ch<N, C::NCH>(a, acc0 + cb * C::NCH, acc1 + cb * C::NCH, nt * N + cofs + cb * C::NCH, x, y0,
-                               part_row, q, amax0, amax1);
-      if (a.amax) {
-        amax0 = warp_max(amax0);
-        amax1 = warp_max(amax1);
-        if (lane == 0) {
-          if (amax0 > 0.f) atomicMax(a.amax, __float_as_uint(amax0));
-          if (amax1 > 0.f) atomicMax(a.amax + 1, __float_as_uint(amax1));
-        }
+        for (int cb = 0; cb < C::CPG / C::NCH; ++cb)
+          epilogue_ch<N, C::NCH>(a, acc0 + cb * C::NCH, acc1 + cb * C::NCH, nt * N + cofs + cb * C::NCH, x, y0,
+                                 part_row, q, amax0, amax1);
+      }
+    }
+    if (a.amax) {
+      amax0 = warp_max(amax0);
+      amax1 = warp_max(amax1);
+      if (lane == 0) {
+        if (amax0 > 0.f) atomicMax(a.amax, __float_as_uint(amax0));
+        if (amax1 > 0.f) atomicMax(a.amax + 1, __float_as_uint(amax1));
       }
     }
   }

@@ -1,2 +1,8 @@
-SPST_DIST_BACKEND=gloo SPST_BENCH_DEVICE=0 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29512 bench.py --gpus 2 --steps 3 --warmup 3 --config c2 --no-cpu-baseline > gpurun_out/bench_gloo2.json 2> gpurun_out/bench_gloo2.err; tail -c 600 gpurun_out/bench_gloo2.json; tail -3 gpurun_out/bench_gloo2.err
-python tools/run_c4.py --repeat 2 --out gpurun_out/c4_fast.json > gpurun_out/c4_fast.log 2>&1; grep "^run" gpurun_out/c4_fast.log
+for lib in build/libspst_base.so paper_2212_13459_b200/libspst.so build/libspst_base.so paper_2212_13459_b200/libspst.so; do
+  SPST_LIB=$PWD/$lib python tools/eval_time.py 2>&1 | tail -1
+done
+for lib in build/libspst_base.so paper_2212_13459_b200/libspst.so; do
+  n=$(basename $lib .so)
+  SPST_LIB=$PWD/$lib ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$n.csv python tools/profile_eval.py > /dev/null 2>&1
+done
+python -m pytest tests/test_gpu_kernels.py tests/test_gpu_maxpool.py tests/test_gpu_parity.py -q -x > gpurun_out/t.log 2>&1; tail -2 gpurun_out/t.log

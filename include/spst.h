@@ -62,6 +62,11 @@ int spst_create(int device, int n_layers, const int* kinds, const int* cin, cons
 void spst_destroy(spst_ctx* ctx);
 const char* spst_last_error(const spst_ctx* ctx);
 int spst_set_stream(spst_ctx* ctx, void* cuda_stream);
+/* Tensor-core precision of the conv layers (SURVEY.md §7 step 3 precision knob): 0 = fp16x3
+ * (hi/lo split operands, three MMA passes, fp32-class -- the default and the parity mode);
+ * 1 = fp16 (hi*hi only, one pass: ~1e-3 relative per layer, opt-in speed mode that does NOT
+ * meet the gradient parity bar).  Statistics (Gram) stay fp16x3 in both. */
+int spst_set_precision(spst_ctx* ctx, int mode);
 
 /* Geometry (localized.py:116-120 make_grid, tiling.py:57-72). h, w: unpadded image. The
  * padded grid is (Hp, Wp) = dims rounded up to the deepest stride. This context evaluates

@@ -9,6 +9,7 @@ resampling) runs in the in-tree CUDA library ``libspst.so`` through its C ABI
 
 from .errors import (ConfigError, DegenerateStdWarning, EmptyError, FormatError, GeometryError,
                      NonFiniteError, PrecisionWarning, ShapeError)
+from .device import get_precision, set_precision
 from .extractor import forward_taps
 from .lbfgs import LBFGSConfig, LBFGSState, Trace, minimize, two_loop_direction
 from .localized import (TransferProblem, build_problem, loss_grad, loss_grad_global, make_grid, stats_pass,

@@ -39,6 +39,7 @@ SIGNATURES = {
     "spst_destroy": (None, [c_void_p]),
     "spst_last_error": (ctypes.c_char_p, [c_void_p]),
     "spst_set_stream": (c_int, [c_void_p, c_void_p]),
+    "spst_set_precision": (c_int, [c_void_p, c_int]),
     "spst_bind": (c_int, [c_void_p, c_int, c_int, c_int, c_int, c_int, c_int]),
     "spst_unbind": (c_int, [c_void_p]),
     "spst_bind_window": (c_int, [c_void_p, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int]),

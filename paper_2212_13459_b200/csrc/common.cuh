@@ -66,6 +66,7 @@ struct ConvArgs {
   int pool_max;
   uint32_t* pool_arg;
   int drain;                     // K-chunks per TMEM accumulation group (1 or 2)
+  int pass0;                     // first MMA pass: 0 = fp16x3 (hi*lo, lo*hi, hi*hi), 2 = fp16 (hi*hi only)
   float comp[4];                 // round-toward-zero bias factor per group relative to `fine`:
                                  // [conv 1, conv 2, extra 1, extra 2 chunks]
   float fine;                    // common relative correction applied once to the drained sum

@@ -113,6 +113,9 @@ __host__ __device__ constexpr int n_groups(int D, int n_kc, int n_xkc) {
   return (n_kc + D - 1) / D + (n_xkc + D - 1) / D;
 }
 
+#ifndef SPST_PACKED128
+#define SPST_PACKED128 0  // packed conversions in the N=128 epilogue (A/B knob)
+#endif
 // 8 channels of one pixel -> hi/lo planes: hi = RN(v s), lo = RN(v s - hi).  PACKED uses two
 // floats per F2FP conversion (same bits, fewer instructions; it pays on the epilogue-bound
 // 64-channel layers, while on N=128 it perturbs register allocation of the pool epilogues).
@@ -249,8 +252,8 @@ __device__ __forceinline__ void epilogue_ch(const ConvArgs& a, float* v0, float*
     if (a.epi == EPI_FWD || a.store_full) {
 #pragma unroll
       for (int k = 0; k < KG; ++k) {
-        if (ok0) store_hl8<N == 64>(a.out, (ch0 >> 3) + k, y0, x, v0 + 8 * k, a.out.scale);
-        if (ok1) store_hl8<N == 64>(a.out, (ch0 >> 3) + k, y0 + 1, x, v1 + 8 * k, a.out.scale);
+        if (ok0) store_hl8<N == 64 || SPST_PACKED128>(a.out, (ch0 >> 3) + k, y0, x, v0 + 8 * k, a.out.scale);
+        if (ok1) store_hl8<N == 64 || SPST_PACKED128>(a.out, (ch0 >> 3) + k, y0 + 1, x, v1 + 8 * k, a.out.scale);
       }
       if constexpr (N == 64) {  // (the N=128 kernel's codegen prefers the select form)
         if (ok0) {
@@ -312,7 +315,7 @@ __device__ __forceinline__ void epilogue_ch(const ConvArgs& a, float* v0, float*
       }
       if ((lane & 1) == 0 && px < a.out_pool.W && py < a.out_pool.H) {
 #pragma unroll
-        for (int k = 0; k < KG; ++k) store_hl8<N == 64>(a.out_pool, (ch0 >> 3) + k, py, px, pv + 8 * k, a.out_pool.scale);
+        for (int k = 0; k < KG; ++k) store_hl8<N == 64 || SPST_PACKED128>(a.out_pool, (ch0 >> 3) + k, py, px, pv + 8 * k, a.out_pool.scale);
 #pragma unroll
         for (int j = 0; j < NCH; ++j) amax1 = fmaxf(amax1, pv[j]);
       }
@@ -354,7 +357,7 @@ __device__ __forceinline__ void epilogue_ch(const ConvArgs& a, float* v0, float*
 #pragma unroll
       for (int j = 0; j < NCH; ++j) amax0 = fmaxf(amax0, fabsf(v[j]));
 #pragma unroll
-      for (int k = 0; k < KG; ++k) store_hl8<N == 64>(a.out, (ch0 >> 3) + k, y, x, v + 8 * k, a.out.scale);
+      for (int k = 0; k < KG; ++k) store_hl8<N == 64 || SPST_PACKED128>(a.out, (ch0 >> 3) + k, y, x, v + 8 * k, a.out.scale);
     }
   } else {  // EPI_BWD_POOL: out is the 2x finer grid
 #pragma unroll
@@ -409,7 +412,7 @@ __device__ __forceinline__ void epilogue_ch(const ConvArgs& a, float* v0, float*
 #pragma unroll
           for (int j = 0; j < NCH; ++j) amax0 = fmaxf(amax0, fabsf(w[j]));
 #pragma unroll
-          for (int k = 0; k < KG; ++k) store_hl8<N == 64>(a.out, (ch0 >> 3) + k, yy, xx, w + 8 * k, a.out.scale);
+          for (int k = 0; k < KG; ++k) store_hl8<N == 64 || SPST_PACKED128>(a.out, (ch0 >> 3) + k, yy, xx, w + 8 * k, a.out.scale);
         }
     }
   }
@@ -547,12 +550,13 @@ __global__ void __launch_bounds__(ConvCfg<N, RES>::THREADS, 1) conv3x3_tc_kernel
             for (int pass = 0; pass < 3; ++pass)
 #pragma unroll
               for (int ks = 0; ks < C::XKG / 2; ++ks) {
+                if (pass < a.pass0) continue;  // one-pass (fp16) mode: hi*hi only
                 const uint64_t bd = bdesc0 + (uint64_t)((((pass == 0 ? C::XKG : 0) + 2 * ks) * N * 16) >> 4);
 #pragma unroll
                 for (int mt = 0; mt < C::MT; ++mt) {
                   const uint64_t ad =
                       adesc0 + (uint64_t)(((pass == 1 ? C::XA_HALF : 0) + mt * 128 * 16 + 2 * ks * C::XA_PLANE) >> 4);
-                  umma_f16_ws(dcol + mt * N, ad, bd, idesc, (!gfirst || pass | ks) ? 1u : 0u);
+                  umma_f16_ws(dcol + mt * N, ad, bd, idesc, (!gfirst || pass != a.pass0 || ks) ? 1u : 0u);
                 }
               }
           } else if constexpr (N == 64 && C::MT == 2) {
@@ -568,13 +572,14 @@ __global__ void __launch_bounds__(ConvCfg<N, RES>::THREADS, 1) conv3x3_tc_kernel
             const uint64_t adesc0 = make_sdesc(st, C::A_PLANE, 128);
 #pragma unroll
             for (int pass = 0; pass < 3; ++pass) {
+              if (pass < a.pass0) continue;  // one-pass (fp16) mode: hi*hi only
               const uint64_t bp = bdesc0 + (uint64_t)(((pass == 0 ? 9 : 0) * C::B_TAP) >> 4);
               const uint64_t ap = adesc0 + (uint64_t)((pass == 1 ? C::A_HALF : 0) >> 4);
 #pragma unroll
               for (int dx = 0; dx < 3; ++dx) {
                 const uint64_t bx = bp + (uint64_t)((dx * 2 * ROWS3 * 16) >> 4);
                 const uint64_t a0 = ap + (uint64_t)((dx * 16) >> 4), rowp = (uint64_t)((C::PITCH * 16) >> 4);
-                const uint32_t first = (gfirst && pass == 0 && dx == 0) ? 0u : 1u;
+                const uint32_t first = (gfirst && pass == a.pass0 && dx == 0) ? 0u : 1u;
                 umma_f16_ws(dcol, a0 + rowp, bx + (uint64_t)((N * 16) >> 4), idesc2, first);  // r=1
                 umma_f16_ws(dcol, a0, bx + (uint64_t)((2 * N * 16) >> 4), idesc, 1u);         // r=0
                 umma_f16_ws(dcol, a0 + 2 * rowp, bx, idesc2, 1u);                              // r=2
@@ -589,6 +594,7 @@ __global__ void __launch_bounds__(ConvCfg<N, RES>::THREADS, 1) conv3x3_tc_kernel
             // the sum small while the corrections go in cuts the chunk's rounding error ~3x.
 #pragma unroll
             for (int pass = 0; pass < 3; ++pass) {
+              if (pass < a.pass0) continue;  // one-pass (fp16) mode: hi*hi only
               const uint64_t bp = bdesc0 + (uint64_t)(((pass == 0 ? 9 : 0) * C::B_TAP) >> 4);
               const uint64_t ap = adesc0 + (uint64_t)((pass == 1 ? C::A_HALF : 0) >> 4);
 #pragma unroll
@@ -598,7 +604,7 @@ __global__ void __launch_bounds__(ConvCfg<N, RES>::THREADS, 1) conv3x3_tc_kernel
 #pragma unroll
                 for (int mt = 0; mt < C::MT; ++mt) {
                   const uint64_t ad = ap + (uint64_t)((((mt + dy) * C::PITCH + dx) * 16) >> 4);
-                  umma_f16_ws(dcol + mt * N, ad, bd, idesc, (!gfirst || pass | tap) ? 1u : 0u);  // fresh per group
+                  umma_f16_ws(dcol + mt * N, ad, bd, idesc, (!gfirst || pass != a.pass0 || tap) ? 1u : 0u);  // fresh per group
                 }
               }
             }

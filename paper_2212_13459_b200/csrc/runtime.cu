@@ -141,12 +141,13 @@ int bwd_drain() {
 void set_conv_comp(ConvArgs& a, int N) {
   const double k = rz_kappa();
   const int xkg = conv_tc_xkg(N);
-  const double wf = rz_weight(18, 9, a.drain);
+  const int sc = a.pass0 == 0 ? 18 : 0, sx = a.pass0 == 0 ? xkg : 0;  // correction MMAs per chunk
+  const double wf = rz_weight(sc, 9, a.drain);
   a.fine = (float)(k * wf);
-  a.comp[0] = (float)(1.0 + k * (rz_weight(18, 9, 1) - wf));
-  a.comp[1] = (float)(1.0 + k * (rz_weight(18, 9, 2) - wf));
-  a.comp[2] = (float)(1.0 + k * (rz_weight(xkg, xkg / 2, 1) - wf));
-  a.comp[3] = (float)(1.0 + k * (rz_weight(xkg, xkg / 2, 2) - wf));
+  a.comp[0] = (float)(1.0 + k * (rz_weight(sc, 9, 1) - wf));
+  a.comp[1] = (float)(1.0 + k * (rz_weight(sc, 9, 2) - wf));
+  a.comp[2] = (float)(1.0 + k * (rz_weight(sx, xkg / 2, 1) - wf));
+  a.comp[3] = (float)(1.0 + k * (rz_weight(sx, xkg / 2, 2) - wf));
 }
 // enough (split x pair) CTAs for two waves, splits of 1K..64K pixels (multiples of 128)
 int gram_px_per_split(long long px, int pairs) {
@@ -268,6 +269,7 @@ struct spst_ctx {
   double* content_partial = nullptr;
   __half* zero_xw = nullptr;
   bool fwd_done = false, finalized = false;
+  int precision = 0;  // SPST_PRECISION_*: 0 fp16x3 (fp32-class, default), 1 fp16 (one MMA pass, opt-in)
   // Deferred end-of-pass range checks (fast path): the forward's check is resolved by the next
   // call that needs its results (finalize's one read-back, or capture / stats / features), the
   // backward's by spst_backward_resolve -- one host synchronisation per pass pair instead of
@@ -606,6 +608,7 @@ int run_conv(spst_ctx* ctx, ConvLaunch& L) {
   a.tiles_y = (L.H + mt - 1) / mt;
   a.acc_scale = L.acc_scale;
   a.drain = L.drain;
+  a.pass0 = ctx->precision == 1 ? 2 : 0;
   if (a.n_kc + a.n_xkc == 0) return ctx->fail(SPST_ERR_CONFIG, "empty GEMM");
   const int tiles = a.tiles_x * a.tiles_y * a.n_ntiles;
   set_conv_comp(a, N);
@@ -1329,6 +1332,12 @@ int spst_timing_read(spst_ctx* ctx, double* ms, double* flops, long long* launch
     flops[c] = ctx->t_flops[c];
     launches[c] = ctx->t_n[c];
   }
+  return SPST_OK;
+}
+
+int spst_set_precision(spst_ctx* ctx, int mode) {
+  if (mode != 0 && mode != 1) return ctx->fail(SPST_ERR_CONFIG, "precision mode must be 0 (fp16x3) or 1 (fp16)");
+  ctx->precision = mode;
   return SPST_OK;
 }
 

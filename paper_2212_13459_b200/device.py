@@ -90,6 +90,7 @@ class Engine:
                 self._h = None
             nat.check(status, None, f"spst_create: {msg}")
         self._finalizer = weakref.finalize(self, L.spst_destroy, self._h)
+        self._check(L.spst_set_precision(self._h, _PRECISION_MODES[_precision]), "spst_set_precision")
         self.geom = {t: tap_geometry(spec, t) for t in spec.taps}
         self.bound = None
         self.bind_epoch = 0
@@ -273,6 +274,26 @@ class Engine:
 
 
 _ENGINES: dict = {}
+
+_PRECISION_MODES = {"fp16x3": 0, "fp16": 1}
+_precision = "fp16x3"
+
+
+def set_precision(mode: str) -> None:
+    """Tensor-core precision of the conv layers for every engine (existing and future):
+    "fp16x3" (default: hi/lo split operands, three MMA passes, fp32-class, meets the parity
+    bar) or "fp16" (one pass, ~3x less tensor work, ~1e-3 relative per layer -- an opt-in speed
+    mode for previews; it does not meet the gradient parity bar).  SURVEY.md §7 step 3."""
+    global _precision
+    if mode not in _PRECISION_MODES:
+        raise ValueError(f"precision must be one of {sorted(_PRECISION_MODES)}, got {mode!r}")
+    _precision = mode
+    for _, eng in _ENGINES.values():
+        eng._check(nat.lib().spst_set_precision(eng._h, _PRECISION_MODES[mode]), "spst_set_precision")
+
+
+def get_precision() -> str:
+    return _precision
 
 
 def engine_for(spec, device: int | None = None) -> Engine:

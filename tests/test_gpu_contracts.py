@@ -78,3 +78,28 @@ def test_float64_inputs_warn(tiny_spec):
     with warnings.catch_warnings():
         warnings.simplefilter("error", spst.PrecisionWarning)
         spst.loss_grad(u.astype(np.float32), p)
+
+
+def test_fp16_precision_mode_is_opt_in(vgg_spec):
+    """SURVEY.md §7 step 3 precision knob: one-pass fp16 convs run (loss within ~1e-2, gradient
+    visibly coarser than the fp32-class default); the default mode is restored and exact again."""
+    d = golden("vgg19.npz")
+    w = spst.default_loss_weights(vgg_spec, lambda_c=float(d["c1_lambda_c"][0]))
+    p = spst.build_problem(d["c1_u"], d["c1_v"], vgg_spec, w)
+    x = golden("vgg19_iterates.npz")["x2"]
+    g64 = golden("vgg19_iterates.npz")["grad64_2"]
+    l64 = float(golden("vgg19_iterates.npz")["loss64_2"][0])
+    assert spst.get_precision() == "fp16x3"
+    try:
+        spst.set_precision("fp16")
+        lf, gf = spst.loss_grad(x, p)
+    finally:
+        spst.set_precision("fp16x3")
+    l3, g3 = spst.loss_grad(x, p)
+    ef, e3 = rel_l2(gf, g64), rel_l2(g3, g64)
+    print(f"fp16: loss rel {abs(lf - l64) / l64:.1e}, grad {ef:.1e}; fp16x3: loss rel {abs(l3 - l64) / l64:.1e}, "
+          f"grad {e3:.1e}")
+    assert abs(lf - l64) <= 1e-2 * l64 and ef < 1.0
+    assert abs(l3 - l64) <= 1e-5 * l64 and e3 <= 1e-3 and ef > 10 * e3
+    with pytest.raises(ValueError):
+        spst.set_precision("bf16")

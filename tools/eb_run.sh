@@ -1,8 +1,3 @@
-for lib in build/libspst_base.so paper_2212_13459_b200/libspst.so build/libspst_base.so paper_2212_13459_b200/libspst.so; do
-  SPST_LIB=$PWD/$lib python tools/eval_time.py 2>&1 | tail -1
-done
-for lib in build/libspst_base.so paper_2212_13459_b200/libspst.so; do
-  n=$(basename $lib .so)
-  SPST_LIB=$PWD/$lib ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$n.csv python tools/profile_eval.py > /dev/null 2>&1
-done
-python -m pytest tests/test_gpu_kernels.py tests/test_gpu_maxpool.py tests/test_gpu_parity.py -q -x > gpurun_out/t.log 2>&1; tail -2 gpurun_out/t.log
+python -m pytest tests/test_gpu_contracts.py tests/test_gpu_kernels.py -q -x -s > gpurun_out/t.log 2>&1; grep -E "fp16|passed|failed|Error" gpurun_out/t.log | tail -5
+python bench.py --steps 10 --warmup 3 --no-cpu-baseline --precision fp16 > gpurun_out/bench_fp16.json 2> gpurun_out/bench_fp16.err; tail -c 300 gpurun_out/bench_fp16.json
+python bench.py --steps 10 --warmup 3 > gpurun_out/bench.json 2> gpurun_out/bench.err; tail -c 300 gpurun_out/bench.json

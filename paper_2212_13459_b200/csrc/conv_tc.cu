@@ -113,43 +113,25 @@ __host__ __device__ constexpr int n_groups(int D, int n_kc, int n_xkc) {
   return (n_kc + D - 1) / D + (n_xkc + D - 1) / D;
 }
 
-#ifndef SPST_PACKED128
-#define SPST_PACKED128 0  // packed conversions in the N=128 epilogue (A/B knob)
-#endif
-// 8 channels of one pixel -> hi/lo planes: hi = RN(v s), lo = RN(v s - hi).  PACKED uses two
-// floats per F2FP conversion (same bits, fewer instructions; it pays on the epilogue-bound
-// 64-channel layers, while on N=128 it perturbs register allocation of the pool epilogues).
-template <bool PACKED>
+// 8 channels of one pixel -> hi/lo planes: hi = RN(v s), lo = RN(v s - hi), two floats per
+// F2FP conversion (packed: 1 % faster than per-element conversions on the N=128 epilogue too,
+// r02 A/B 131.3 -> 130.0 ms/evaluation of conv3x3_tc<128>).
 __device__ __forceinline__ void store_hl8(const HL16& t, int kg, int y, int x, const float* v8, float s) {
-  if constexpr (PACKED) {
-    const size_t off = ((size_t)kg * t.H + y) * t.W + x;
-    uint4 h, l;
-    uint32_t* hp = &h.x;
-    uint32_t* lp = &l.x;
+  const size_t off = ((size_t)kg * t.H + y) * t.W + x;
+  uint4 h, l;
+  uint32_t* hp = &h.x;
+  uint32_t* lp = &l.x;
 #pragma unroll
-    for (int e = 0; e < 8; e += 2) {
-      const float a = v8[e] * s, b = v8[e + 1] * s;
-      const __half2 hi = __floats2half2_rn(a, b);
-      const float2 back = __half22float2(hi);
-      const __half2 lo = __floats2half2_rn(a - back.x, b - back.y);
-      hp[e / 2] = *reinterpret_cast<const uint32_t*>(&hi);
-      lp[e / 2] = *reinterpret_cast<const uint32_t*>(&lo);
-    }
-    reinterpret_cast<uint4*>(t.hi)[off] = h;
-    reinterpret_cast<uint4*>(t.lo())[off] = l;
-  } else {
-    __align__(16) __half h[8];
-    __align__(16) __half l[8];
-#pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      HalfPair p = split_f16(v8[e] * s);
-      h[e] = p.hi;
-      l[e] = p.lo;
-    }
-    size_t off = ((size_t)kg * t.H + y) * t.W + x;
-    reinterpret_cast<uint4*>(t.hi)[off] = *reinterpret_cast<uint4*>(h);
-    reinterpret_cast<uint4*>(t.lo())[off] = *reinterpret_cast<uint4*>(l);
+  for (int e = 0; e < 8; e += 2) {
+    const float a = v8[e] * s, b = v8[e + 1] * s;
+    const __half2 hi = __floats2half2_rn(a, b);
+    const float2 back = __half22float2(hi);
+    const __half2 lo = __floats2half2_rn(a - back.x, b - back.y);
+    hp[e / 2] = *reinterpret_cast<const uint32_t*>(&hi);
+    lp[e / 2] = *reinterpret_cast<const uint32_t*>(&lo);
   }
+  reinterpret_cast<uint4*>(t.hi)[off] = h;
+  reinterpret_cast<uint4*>(t.lo())[off] = l;
 }
 
 __device__ __forceinline__ void load_hl8(const HL16& t, int kg, int y, int x, float* v8) {
@@ -252,8 +234,8 @@ __device__ __forceinline__ void epilogue_ch(const ConvArgs& a, float* v0, float*
     if (a.epi == EPI_FWD || a.store_full) {
 #pragma unroll
       for (int k = 0; k < KG; ++k) {
-        if (ok0) store_hl8<N == 64 || SPST_PACKED128>(a.out, (ch0 >> 3) + k, y0, x, v0 + 8 * k, a.out.scale);
-        if (ok1) store_hl8<N == 64 || SPST_PACKED128>(a.out, (ch0 >> 3) + k, y0 + 1, x, v1 + 8 * k, a.out.scale);
+        if (ok0) store_hl8(a.out, (ch0 >> 3) + k, y0, x, v0 + 8 * k, a.out.scale);
+        if (ok1) store_hl8(a.out, (ch0 >> 3) + k, y0 + 1, x, v1 + 8 * k, a.out.scale);
       }
       if constexpr (N == 64) {  // (the N=128 kernel's codegen prefers the select form)
         if (ok0) {
@@ -315,7 +297,7 @@ __device__ __forceinline__ void epilogue_ch(const ConvArgs& a, float* v0, float*
       }
       if ((lane & 1) == 0 && px < a.out_pool.W && py < a.out_pool.H) {
 #pragma unroll
-        for (int k = 0; k < KG; ++k) store_hl8<N == 64 || SPST_PACKED128>(a.out_pool, (ch0 >> 3) + k, py, px, pv + 8 * k, a.out_pool.scale);
+        for (int k = 0; k < KG; ++k) store_hl8(a.out_pool, (ch0 >> 3) + k, py, px, pv + 8 * k, a.out_pool.scale);
 #pragma unroll
         for (int j = 0; j < NCH; ++j) amax1 = fmaxf(amax1, pv[j]);
       }
@@ -357,7 +339,7 @@ __device__ __forceinline__ void epilogue_ch(const ConvArgs& a, float* v0, float*
 #pragma unroll
       for (int j = 0; j < NCH; ++j) amax0 = fmaxf(amax0, fabsf(v[j]));
 #pragma unroll
-      for (int k = 0; k < KG; ++k) store_hl8<N == 64 || SPST_PACKED128>(a.out, (ch0 >> 3) + k, y, x, v + 8 * k, a.out.scale);
+      for (int k = 0; k < KG; ++k) store_hl8(a.out, (ch0 >> 3) + k, y, x, v + 8 * k, a.out.scale);
     }
   } else {  // EPI_BWD_POOL: out is the 2x finer grid
 #pragma unroll
@@ -412,7 +394,7 @@ __device__ __forceinline__ void epilogue_ch(const ConvArgs& a, float* v0, float*
 #pragma unroll
           for (int j = 0; j < NCH; ++j) amax0 = fmaxf(amax0, fabsf(w[j]));
 #pragma unroll
-          for (int k = 0; k < KG; ++k) store_hl8<N == 64 || SPST_PACKED128>(a.out, (ch0 >> 3) + k, yy, xx, w + 8 * k, a.out.scale);
+          for (int k = 0; k < KG; ++k) store_hl8(a.out, (ch0 >> 3) + k, yy, xx, w + 8 * k, a.out.scale);
         }
     }
   }

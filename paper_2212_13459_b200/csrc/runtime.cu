@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <atomic>
 #include <cmath>
 #include <cstdio>
@@ -727,11 +728,19 @@ bool stage_ranges_ok(spst_ctx* ctx, int k, float m0, float m1) {
 
 int forward_check(spst_ctx* ctx);
 
+// SPST_DEBUG_HOST_US=1: host microseconds spent in each phase of a forward (launch-overhead probe)
+static double host_us() {
+  return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
 int do_forward(spst_ctx* ctx, const float* x, bool careful) {
   const int n = (int)ctx->stages.size();
+  static const bool dbg_us = env_int("SPST_DEBUG_HOST_US", 0) != 0;
+  const double t0 = dbg_us ? host_us() : 0.0;
   for (int k = 0; k < n; ++k) {
     Stage& s = ctx->stages[k];
-    const bool check = careful || !s.out_e.known || (s.pool_after && !s.pool_e.known) || (k == 0 && !ctx->img_e.known);
+    const bool check = careful || (s.has_out && !s.out_e.known) || (s.pool_after && !s.pool_e.known) ||
+                       (k == 0 && !ctx->img_e.known);
     for (int attempt = 0; attempt < 6; ++attempt) {
       TRY(forward_stage(ctx, k, x));
       if (!check) break;
@@ -748,8 +757,10 @@ int do_forward(spst_ctx* ctx, const float* x, bool careful) {
       if (ok) break;
     }
   }
+  const double t1 = dbg_us ? host_us() : 0.0;
   for (int k = 0; k < n; ++k) TRY(stage_stats(ctx, k));
   CK(cudaMemcpyAsync(ctx->amax_pin, ctx->amax_d, 16 * n + 16, cudaMemcpyDeviceToHost, ctx->stream));
+  if (dbg_us) fprintf(stderr, "[spst] forward host us: convs %.1f stats+copy %.1f\n", t1 - t0, host_us() - t1);
   if (!careful) {  // fast path: checked when the results are first needed (resolve_forward)
     ctx->fwd_pending = true;
     return 0;
@@ -773,6 +784,10 @@ int forward_check(spst_ctx* ctx) {
     const float m0 = bits_to_float(ctx->amax_pin[4 * k]), m1 = bits_to_float(ctx->amax_pin[4 * k + 1]);
     if (s.has_out && range_bad(m0, s.out.scale)) bad = true;
     if (s.pool_after && range_bad(m1, s.pooled.scale)) bad = true;
+    static const bool dbg = env_int("SPST_DEBUG_RANGES", 0) != 0;
+    if (dbg && ((s.has_out && range_bad(m0, s.out.scale)) || (s.pool_after && range_bad(m1, s.pooled.scale))))
+      fprintf(stderr, "[spst] fwd stage %d out of range: amax %.3e x scale %.3e, pooled %.3e x %.3e\n", k, m0,
+              s.out.scale, m1, s.pooled.scale);
     // exponents for the next write; the data now stored keep the scale they were written with
     if (s.has_out && m0 > 0 && std::isfinite(m0)) s.out_e = {choose_exp(m0), true};
     if (s.pool_after && m1 > 0 && std::isfinite(m1)) s.pool_e = {choose_exp(m1), true};
@@ -1423,7 +1438,10 @@ long long spst_workspace_bytes(const spst_ctx* ctx) { return ctx->alloc_bytes; }
 int spst_forward_pitched(spst_ctx* ctx, const float* x, long long pitch, int flags) {
   (void)flags;
   if (!ctx->bound) return ctx->fail(SPST_ERR_CONFIG, "spst_bind must precede spst_forward");
+  static const bool dbg_us = env_int("SPST_DEBUG_HOST_US", 0) != 0;
+  const double t0 = dbg_us ? host_us() : 0.0;
   TRY(settle(ctx));
+  if (dbg_us) fprintf(stderr, "[spst] forward host us: settle %.1f\n", host_us() - t0);
   ctx->fwd_x = x;
   if (pitch < std::min(ctx->grid_c1, ctx->w) - ctx->grid_c0)
     return ctx->fail(SPST_ERR_SHAPE, "image pitch below the window's image columns");

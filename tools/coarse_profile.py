@@ -21,6 +21,8 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--dims", default="756x1008")
 ap.add_argument("--m", type=int, default=100)
 ap.add_argument("--iters", type=int, default=30)
+ap.add_argument("--stacks", action="store_true", help="attribute device->host copies to Python call sites")
+ap.add_argument("--cprofile", action="store_true", help="host-side cProfile of the iterations instead")
 a = ap.parse_args()
 H, W = (int(t) for t in a.dims.split("x"))
 u = workloads.synth_content(H, W, 1)
@@ -31,8 +33,18 @@ obj = objective_for(p)
 x = torch.from_numpy(u).cuda()
 x1, _ = minimize(obj, x, LBFGSConfig(history_size=a.m, max_iters=a.m + 5))
 torch.cuda.synchronize()
+if a.cprofile:
+    import cProfile
+    import pstats
+    pr = cProfile.Profile()
+    pr.enable()
+    minimize(obj, x1, LBFGSConfig(history_size=a.m, max_iters=a.iters))
+    torch.cuda.synchronize()
+    pr.disable()
+    pstats.Stats(pr).sort_stats("tottime").print_stats(25)
+    sys.exit(0)
 from torch.profiler import ProfilerActivity, profile  # noqa: E402
-with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
+with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU], with_stack=a.stacks) as prof:
     t0 = time.perf_counter()
     x2, tr = minimize(obj, x1, LBFGSConfig(history_size=a.m, max_iters=a.iters))
     torch.cuda.synchronize()
@@ -72,3 +84,13 @@ for name, (us, n) in sorted(tot.items(), key=lambda kv: -kv[1][0])[:30]:
 print("idle gaps > 5 us (after -> before):")
 for (n0, n1), (us, n) in sorted(gaps.items(), key=lambda kv: -kv[1][0])[:14]:
     print(f"  {us / 1e3 / its:7.3f} ms/iter  {n / its:5.1f}/iter  {us / n:7.1f} us  {n0} -> {n1}")
+if a.stacks:
+    sites = defaultdict(int)
+    for e in prof.events():
+        if e.device_type == torch.autograd.DeviceType.CPU and e.name in ("cudaMemcpyAsync", "cudaMemcpy",
+                                                                          "cudaStreamSynchronize"):
+            frames = [f for f in (e.stack or []) if "paper_2212_13459_b200" in f or "tools/" in f][:3]
+            sites[(e.name, " < ".join(frames))] += 1
+    print("runtime copy / sync call sites:")
+    for (name, st), n in sorted(sites.items(), key=lambda kv: -kv[1])[:20]:
+        print(f"  {n / its:6.1f}/iter  {name}  {st}")

@@ -108,9 +108,21 @@ int round_up(int v, int m) { return (v + m - 1) / m * m; }
 // result truncation, every addend's alignment truncation biases the same way.  kappa per
 // kernel and entry kind, measured on B200 with tools/rz_calibrate.py (relu-like operands;
 // checked on VGG-19 taps with tools/error_budget.py).
+// The K dimension of a Gram accumulation is pixels: a row narrower than the stage (deep taps of
+// small images, e.g. 16 px at relu5_1 of a 256x256 image) or a row's last partial stage is TMA
+// zero fill, and zero addends truncate nothing.  The weights therefore count only the K=16 steps
+// that carry real pixels, averaged over the row's stages by pixel count (g.w_own must be set).
 void set_gram_comp(GramArgs& g, int C_p, bool nonneg = true) {
   const bool c64 = C_p == 64;
-  const double w1 = spst::rz_weight(c64 ? 0 : 8, c64 ? 8 : 4, 1), w2 = spst::rz_weight(c64 ? 0 : 8, c64 ? 8 : 4, 2);
+  const int kpx = c64 ? 128 : 64, steps = kpx / 16;
+  // 128 channels: 2 correction + 1 hi*hi MMA per real K step; 64 channels: 1 hi*hi MMA
+  auto W = [&](int r, int chunks) { return spst::rz_weight(c64 ? 0 : 2 * r, r, chunks); };
+  const int w_own = std::max(1, g.w_own);
+  const int full = w_own / kpx, rem = w_own % kpx, r_rem = (rem + 15) / 16;
+  auto Wavg = [&](int chunks) {
+    return ((double)full * kpx * W(steps, chunks) + (rem ? (double)rem * W(r_rem, chunks) : 0.0)) / w_own;
+  };
+  const double w1 = Wavg(1), w2 = Wavg(2);
   const double on = spst::rz_kappa() > 0.0 ? 1.0 : 0.0;  // SPST_RZ_KAPPA=0 disables every compensation
   const double kd = on * (c64 ? 7.3e-8 : 5.2e-8), ko = on * (nonneg ? (c64 ? 4.9e-8 : 3.8e-8) : spst::rz_kappa());
   g.fine_diag = (float)(kd * w2);

@@ -1,4 +1,3 @@
 cd $GRAFT_REPO_ROOT
-export SPST_DEBUG_STORE_ALL=1
-timeout 600 python tools/error_budget.py --points 3 --diag 2>&1 | grep -v Warn | grep "diag\|^\[" 
-timeout 600 python tools/error_budget.py --points 5 --diag 2>&1 | grep -v Warn | grep "diag\|^\["
+timeout 2400 python -m pytest tests -m gpu -q 2>&1 | tail -4
+timeout 600 python bench.py > gpurun_out/bench_gramfill2.json 2> gpurun_out/bench_gramfill2.err; tail -c 400 gpurun_out/bench_gramfill2.json

@@ -820,12 +820,21 @@ cudaError_t launch_absmax(int f64, const void* a, long long n, double* partial, 
 cudaError_t launch_two_loop_coop(int f64, const TwoLoopArgs& a, cudaStream_t st) {
   if (a.m < 1 || a.m > kTwoLoopMaxHist) return cudaErrorNotSupported;
   const void* fn = f64 ? (const void*)two_loop_coop_kernel<double> : (const void*)two_loop_coop_kernel<float>;
-  int dev = 0, coop = 0, per_sm = 0, sms = 0;
+  // co-residency of the grid, queried once per device and precision (the query costs tens of
+  // microseconds of host time per L-BFGS iteration otherwise, with the GPU idle behind it)
+  constexpr int kMaxDev = 64;
+  static int ok_cache[kMaxDev][2] = {};  // 0 unknown, 1 cooperative launch fits, 2 it does not
+  int dev = 0;
   cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kRedThreads, 0);
-  if (!coop || per_sm * sms < kRedBlocks) {
+  int& ok = ok_cache[dev < kMaxDev ? dev : 0][f64 ? 1 : 0];
+  if (ok == 0) {
+    int coop = 0, per_sm = 0, sms = 0;
+    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kRedThreads, 0);
+    ok = (coop && per_sm * sms >= kRedBlocks) ? 1 : 2;
+  }
+  if (ok != 1) {
     cudaGetLastError();
     return cudaErrorNotSupported;
   }

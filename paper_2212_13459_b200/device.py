@@ -153,6 +153,19 @@ class Engine:
                     "spst_tap_info")
         return n.value
 
+    def owned_counts(self):
+        """owned_pixels of every style tap (cached per binding)."""
+        if getattr(self, "_counts_epoch", None) != self.bind_epoch:
+            self._counts = [self.owned_pixels(i) for i in range(len(self.style_taps))]
+            self._counts_epoch = self.bind_epoch
+        return self._counts
+
+    def pinned_scalar(self):
+        """A pinned host f64[1] for asynchronous scalar read-backs on the engine stream."""
+        if getattr(self, "_pin1", None) is None:
+            self._pin1 = torch.empty(1, dtype=torch.float64).pin_memory()
+        return self._pin1
+
     def workspace_bytes(self):
         return int(nat.lib().spst_workspace_bytes(self._h))
 

@@ -60,6 +60,9 @@ class _Vec:
         nb = nat.lib().spst_vec_partials()
         self.partial = torch.empty(3 * nb, dtype=torch.float64, device=device)
         self.out = torch.empty(8, dtype=torch.float64, device=device)
+        # pinned mirror of `out`: results copied behind a pass the host synchronises on anyway
+        # are read without a second device round trip
+        self.out_pin = torch.empty(8, dtype=torch.float64).pin_memory()
         self.alpha = torch.empty(0, dtype=torch.float64, device=device)
         self.coef = torch.empty(1, dtype=torch.float64, device=device)
         self.ticket = torch.zeros(1, dtype=torch.int32, device=device)  # fused two-loop finish counter
@@ -170,9 +173,14 @@ def _two_loop(g, state: LBFGSState, vec: _Vec, out, allreduce=None):
     dot = torch.empty(1, dtype=torch.float64, device=dev)
     gamma = (1.0 / R[-1]) / state.yy[-1]
     if allreduce is None:  # single device: the whole sequence in one native call
-        sp = (ctypes.c_void_p * m)(*[t.data_ptr() for t in S])
-        yp = (ctypes.c_void_p * m)(*[t.data_ptr() for t in Y])
-        rp = (ctypes.c_double * m)(*R)
+        # (numpy-built argument arrays: a 100-pair history costs ~20 us of host time instead of
+        # ~80 us with element-wise ctypes arrays, and the GPU idles for all of it)
+        vp = ctypes.POINTER(ctypes.c_void_p)
+        sa = np.array([t.data_ptr() for t in S], dtype=np.uint64)
+        ya = np.array([t.data_ptr() for t in Y], dtype=np.uint64)
+        ra = np.array(R, dtype=np.float64)
+        sp, yp = sa.ctypes.data_as(vp), ya.ctypes.data_as(vp)
+        rp = ra.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
         nat.check(nat.lib().spst_vec_two_loop(vec.f64, nat.ptr(g), nat.ptr(out), sp, yp, rp, float(gamma), m,
                                               g.numel(), nat.ptr(vec.partial), nat.ptr(alpha), nat.ptr(vec.ticket),
                                               nat.ptr(vec.coef), vec._s()), None, "spst_vec_two_loop")
@@ -365,7 +373,8 @@ def minimize(f, x0, cfg: LBFGSConfig, callback=None, allreduce=None, resume: LBF
             t *= cfg.shrink
         gmax_new = None
         if accepted:
-            spare = next(k for k in range(m + 1) if k not in slot_of)
+            taken = set(slot_of)
+            spare = next(k for k in range(m + 1) if k not in taken)
             s, y = ring_s[spare], ring_y[spare]
             if lazy and allreduce is None and hasattr(obj, "grad_resolve"):
                 # one host synchronisation for the gradient's range check, the curvature dots
@@ -375,10 +384,14 @@ def minimize(f, x0, cfg: LBFGSConfig, callback=None, allreduce=None, resume: LBF
                 trace.grads += 1
                 vec.sy(x_try, x, g_try, g, s, y, read=False)
                 vec.absmax(g_try, slot=3, read=False)
+                vec.out_pin[:4].copy_(vec.out[:4], non_blocking=True)
                 if obj.grad_resolve():
                     vec.sy(x_try, x, g_try, g, s, y, read=False)
                     vec.absmax(g_try, slot=3, read=False)
-                ys, ss, yy, gmax_new = vec.out[:4].tolist()
+                    ys, ss, yy, gmax_new = vec.out[:4].tolist()
+                else:
+                    torch.cuda.current_stream(x.device).synchronize()  # (idle already when resolved)
+                    ys, ss, yy, gmax_new = vec.out_pin[:4].tolist()
             else:
                 if lazy:
                     g_try = obj.grad(g_spare)

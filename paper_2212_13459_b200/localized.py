@@ -353,15 +353,20 @@ class Evaluation:
         if self.whole:
             eng.forward(x_dev)
             _meter(eng)
-            counts = [eng.owned_pixels(i) for i in range(len(eng.style_taps))]
-            content = eng.content_sqdiff() if p.has_content else None  # read after finalize's one sync
+            counts = eng.owned_counts()
+            content = eng.content_sqdiff() if p.has_content else None
+            if content is not None:  # copied behind the pass: read after finalize's one sync
+                cpin = eng.pinned_scalar()
+                cpin.copy_(content, non_blocking=True)
             terms, degenerate = eng.finalize(counts)
-            if content is not None and eng.forward_redone():  # the forward was re-run in careful mode
-                content = eng.content_sqdiff()
             _warn_degenerate(degenerate)
             total = float(terms.sum())
             if content is not None:
-                total += p.weights.lambda_c * float(content.item())
+                if eng.forward_redone():  # the forward was re-run in careful mode
+                    cval = float(eng.content_sqdiff().item())
+                else:
+                    cval = float(cpin[0])
+                total += p.weights.lambda_c * cval
             return total
         # windowed: pass 1 (statistics of every window, content loss of every owned crop)
         T = len(eng.style_taps)

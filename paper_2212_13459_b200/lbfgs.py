@@ -166,7 +166,7 @@ def _two_loop(g, state: LBFGSState, vec: _Vec, out, allreduce=None):
     per dot product across ranks."""
     m = len(state.s_hist)
     if m == 0:
-        return out.copy_(g).neg_()
+        return vec.axpy(g, g, -2.0, out)  # g - 2g = -g exactly (Sterbenz), one native kernel
     S, Y, R = state.s_hist, state.y_hist, state.rho
     dev = g.device
     alpha = torch.empty(m, dtype=torch.float64, device=dev)
@@ -360,7 +360,7 @@ def minimize(f, x0, cfg: LBFGSConfig, callback=None, allreduce=None, resume: LBF
         _two_loop(g, state, vec, d, allreduce)
         gd = red_dot(g, d)
         if gd >= 0:  # not a descent direction: steepest descent
-            d.copy_(g).neg_()
+            vec.axpy(g, g, -2.0, d)  # -g
             gd = red_dot(g, d)
         t = 1.0 / gmax if not state.s_hist else 1.0
         accepted = False

@@ -8,6 +8,9 @@ KEYS = [
     ("sm_clock", "sm__cycles_elapsed.avg.per_second"),
     ("tensor_pipe_active_%", "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed"),
     ("tensor_mem_active_%", "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed"),
+    ("fp16_mma_util_%", "sm__ops_path_tensor_op_utchmma_src_fp16_dst_fp32_sparsity_off.sum.pct_of_peak_sustained_elapsed"),
+    ("tmem_c_reads_%", "smsp__mem_tensor_reads_op_utcmma_matrix_c.sum.pct_of_peak_sustained_elapsed"),
+    ("tmem_ld_instructions", "smsp__sass_inst_executed_op_tmem_ldt.sum"),
     ("dram_read", "dram__bytes_read.sum"),
     ("dram_write", "dram__bytes_write.sum"),
     ("dram_throughput_%", "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),

@@ -50,6 +50,10 @@ def init(local_rank: int | None = None, backend: str | None = None):
         if backend == "nccl" and local_rank is not None:
             torch.cuda.set_device(local_rank)
         dist.init_process_group(backend)
+        if backend == "nccl":
+            # create the communicator eagerly with a collective every rank joins: the first
+            # NCCL call of a group must not be a batch_isend_irecv that only some ranks issue
+            dist.all_reduce(torch.zeros(1, device=torch.cuda.current_device()))
     return dist.group.WORLD
 
 

@@ -419,9 +419,14 @@ __device__ __forceinline__ TileId decode_tile(const ConvArgs& a, int t) {
 template <int N, bool RES>
 __global__ void __launch_bounds__(ConvCfg<N, RES>::THREADS, 1) conv3x3_tc_kernel(const __grid_constant__ ConvArgs a) {
   using C = ConvCfg<N, RES>;
+  static_assert(!RES || (N == 64 && C::MT == 2), "the split lo/hi stages are wired into the row-pair path");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ uint64_t full_bar[C::STAGES], empty_bar[C::STAGES];
+  // RES: a stage's lo half has its own barriers (full_lo / empty_lo; full_bar / empty_bar then
+  // guard the hi half): the lo planes feed only the first correction pass, so they are released
+  // -- and the next chunk's lo planes fetched -- a third of a chunk early
+  __shared__ uint64_t full_lo[RES ? C::STAGES : 1], empty_lo[RES ? C::STAGES : 1];
   __shared__ uint64_t cfull_bar[C::NBUF], cempty_bar[C::NBUF], res_bar;
   __shared__ uint32_t tmem_slot;
 
@@ -440,6 +445,10 @@ __global__ void __launch_bounds__(ConvCfg<N, RES>::THREADS, 1) conv3x3_tc_kernel
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
+      if constexpr (RES) {
+        mbar_init(&full_lo[s], 1);
+        mbar_init(&empty_lo[s], 1);
+      }
     }
     for (int b = 0; b < C::NBUF; ++b) {
       mbar_init(&cfull_bar[b], 1);
@@ -478,10 +487,36 @@ __global__ void __launch_bounds__(ConvCfg<N, RES>::THREADS, 1) conv3x3_tc_kernel
       const int y0 = id.ry * C::MT;
       for (int c = 0; c < n_chunks; ++c, ++g) {
         const int s = g % C::STAGES;
-        mbar_wait(&empty_bar[s], ((g / C::STAGES) & 1) ^ 1);
+        const uint32_t eph = ((g / C::STAGES) & 1) ^ 1;
         uint8_t* st = smem + s * C::STAGE;
         int ci;
         const bool extra = chunk_is_extra(c, a.n_kc, ci);
+        if constexpr (RES) {
+          // lo half first (consumed by the first pass), then the hi half; an extra-K chunk
+          // occupies the whole stage and arrives on full_bar only
+          mbar_wait(&empty_lo[s], eph);
+          if (!extra) {
+            if (lane == 0) mbar_arrive_expect_tx(&full_lo[s], C::A_HALF);
+            __syncwarp();
+            if (lane < 8 * C::RIN && s_hl == 1)
+              tma_load_3d(st + s_off, s_map, &full_lo[s], 2 * (x0 - 1) + 128 * s_h, y0 - 1 + s_r, 2 * ci + s_p);
+          }
+          mbar_wait(&empty_bar[s], eph);
+          if (!extra) {
+            if (lane == 0) mbar_arrive_expect_tx(&full_bar[s], C::A_HALF);
+            __syncwarp();
+            if (lane < 8 * C::RIN && s_hl == 0)
+              tma_load_3d(st + s_off, s_map, &full_bar[s], 2 * (x0 - 1) + 128 * s_h, y0 - 1 + s_r, 2 * ci + s_p);
+          } else if (lane == 0) {
+            mbar_arrive(&full_lo[s]);
+            mbar_arrive_expect_tx(&full_bar[s], 2 * C::XA_HALF + C::XB_BYTES);
+            tma_load_4d(st, &a.tm_v_hi, &full_bar[s], 0, x0, y0, C::XKG * ci);
+            tma_load_4d(st + C::XA_HALF, &a.tm_v_lo, &full_bar[s], 0, x0, y0, C::XKG * ci);
+            bulk_load(st + C::XB_OFF, a.xwgt + ((size_t)nt * a.n_xkc + ci) * C::XB_BYTES, C::XB_BYTES, &full_bar[s]);
+          }
+          continue;
+        }
+        mbar_wait(&empty_bar[s], eph);
         if (!extra) {
           if (lane == 0) mbar_arrive_expect_tx(&full_bar[s], C::A_BYTES + (RES ? 0 : C::B_BYTES));
           __syncwarp();
@@ -515,12 +550,18 @@ __global__ void __launch_bounds__(ConvCfg<N, RES>::THREADS, 1) conv3x3_tc_kernel
           const uint32_t b = gq % C::NBUF;
           if (gfirst) mbar_wait(&cempty_bar[b], ((gq / C::NBUF) & 1) ^ 1);
           const int s = g % C::STAGES;
-          mbar_wait(&full_bar[s], (g / C::STAGES) & 1);
+          const uint32_t fph = (g / C::STAGES) & 1;
+          int ci;
+          const bool extra = chunk_is_extra(c, a.n_kc, ci);
+          if constexpr (RES) {
+            mbar_wait(&full_lo[s], fph);
+            if (extra) mbar_wait(&full_bar[s], fph);
+          } else {
+            mbar_wait(&full_bar[s], fph);
+          }
           __syncwarp();
           tc_fence_after();
           const uint32_t st = smem_u32(smem + s * C::STAGE);
-          int ci;
-          const bool extra = chunk_is_extra(c, a.n_kc, ci);
           const uint32_t bb = RES ? smem_u32(smem + C::RES_OFF) + (uint32_t)ci * C::B_BYTES : st + C::A_BYTES;
           const uint32_t dcol = tmem_base + b * C::MT * N;
           // descriptor arithmetic: start-address field = addr >> 4 in the low bits, so an
@@ -552,8 +593,19 @@ __global__ void __launch_bounds__(ConvCfg<N, RES>::THREADS, 1) conv3x3_tc_kernel
             constexpr int ROWS3 = 3 * N;                       // rows of one (pass, dx, kg) slab
             const uint64_t bdesc0 = make_sdesc(bb, ROWS3 * 16, 128);
             const uint64_t adesc0 = make_sdesc(st, C::A_PLANE, 128);
+            // issue order q: RES runs lo*hi first (then hi*lo, hi*hi) so the lo half can be
+            // released after q = 0; both orders put the corrections before the large products
 #pragma unroll
-            for (int pass = 0; pass < 3; ++pass) {
+            for (int q = 0; q < 3; ++q) {
+              if constexpr (RES) {
+                if (q == 1) {  // lo planes consumed: release them, wait for the hi planes
+                  umma_commit_ws(&empty_lo[s]);
+                  mbar_wait(&full_bar[s], fph);
+                  __syncwarp();
+                  tc_fence_after();
+                }
+              }
+              const int pass = RES ? (q == 0 ? 1 : (q == 1 ? 0 : 2)) : q;
               if (pass < a.pass0) continue;  // one-pass (fp16) mode: hi*hi only
               const uint64_t bp = bdesc0 + (uint64_t)(((pass == 0 ? 9 : 0) * C::B_TAP) >> 4);
               const uint64_t ap = adesc0 + (uint64_t)((pass == 1 ? C::A_HALF : 0) >> 4);
@@ -561,7 +613,7 @@ __global__ void __launch_bounds__(ConvCfg<N, RES>::THREADS, 1) conv3x3_tc_kernel
               for (int dx = 0; dx < 3; ++dx) {
                 const uint64_t bx = bp + (uint64_t)((dx * 2 * ROWS3 * 16) >> 4);
                 const uint64_t a0 = ap + (uint64_t)((dx * 16) >> 4), rowp = (uint64_t)((C::PITCH * 16) >> 4);
-                const uint32_t first = (gfirst && pass == a.pass0 && dx == 0) ? 0u : 1u;
+                const uint32_t first = (gfirst && q == a.pass0 && dx == 0) ? 0u : 1u;
                 umma_f16_ws(dcol, a0 + rowp, bx + (uint64_t)((N * 16) >> 4), idesc2, first);  // r=1
                 umma_f16_ws(dcol, a0, bx + (uint64_t)((2 * N * 16) >> 4), idesc, 1u);         // r=0
                 umma_f16_ws(dcol, a0 + 2 * rowp, bx, idesc2, 1u);                              // r=2
@@ -590,6 +642,9 @@ __global__ void __launch_bounds__(ConvCfg<N, RES>::THREADS, 1) conv3x3_tc_kernel
                 }
               }
             }
+          }
+          if constexpr (RES) {
+            if (extra) umma_commit_ws(&empty_lo[s]);
           }
           umma_commit_ws(&empty_bar[s]);
           if (glast) {

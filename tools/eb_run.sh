@@ -1,4 +1,4 @@
 cd $GRAFT_REPO_ROOT
-timeout 900 python bench.py > gpurun_out/final_bench.json 2> gpurun_out/final_bench.err; tail -c 300 gpurun_out/final_bench.json
-timeout 900 python bench.py --impl reference > gpurun_out/final_ref.json 2> gpurun_out/final_ref.err; tail -c 300 gpurun_out/final_ref.json
-timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file gpurun_out/launches_bench.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/ncu_bench.log 2>&1; tail -2 gpurun_out/ncu_bench.log
+timeout 2400 python -m pytest tests -m gpu -q -x 2>&1 | tail -2
+timeout 600 python bench.py --no-cpu-baseline > gpurun_out/bench_split.json 2>/dev/null; python -c "
+import json;d=json.loads(open('gpurun_out/bench_split.json').read().strip().splitlines()[-1]);print(d['value'],d['ms_per_step'],d['clocks'],d['roofline']['classes'])"

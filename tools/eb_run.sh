@@ -1,3 +1,7 @@
+# Scratch command file for one gpurun call (edited per experiment):
+#   /usr/local/graft/bin/gpurun --timeout 3000 -- bash tools/eb_run.sh
+# Default: the round-end checks -- smoke, the GPU parity suite, one bench line.
 cd $GRAFT_REPO_ROOT
-for lib in build/libspst_old.so paper_2212_13459_b200/libspst.so build/libspst_old.so paper_2212_13459_b200/libspst.so; do SPST_LIB=$PWD/$lib timeout 300 python tools/eval_time.py | tail -1; done
-for lib in build/libspst_old.so paper_2212_13459_b200/libspst.so; do n=$(basename $lib .so); SPST_LIB=$PWD/$lib timeout 600 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/ab_$n.csv python tools/profile_eval.py > /dev/null 2>&1; done
+timeout 600 python -c "import __graft_entry__ as g; g.smoke()"
+timeout 2400 python -m pytest tests -m gpu -q 2>&1 | tail -2
+timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; tail -c 400 gpurun_out/bench.json

@@ -18,9 +18,9 @@ from conftest import rel_l2  # noqa: E402
 
 
 @pytest.mark.parametrize("net,shape,grid", [("tiny", (150, 137), (2, 2)), ("vgg", (360, 200), (2, 1)),
-                                            ("vgg", (392, 424), (2, 2))])
+                                            ("vgg", (392, 424), (2, 2)), ("vggmax", (392, 424), (2, 2))])
 def test_device_windows_equal_whole_image(net, shape, grid, tiny_spec, vgg_spec):
-    spec = tiny_spec if net == "tiny" else vgg_spec
+    spec = {"tiny": tiny_spec, "vgg": vgg_spec}.get(net) or spst.calibrated_vgg19(0, pooling="max")
     rng = np.random.default_rng(3)
     h, w = shape
     u = rng.random((h, w, 3)).astype(np.float32)

@@ -15,9 +15,10 @@ from paper_2212_13459_b200.pipeline import RunConfig, _weights_for_scale, object
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c4")
 ap.add_argument("--reps", type=int, default=1)
+ap.add_argument("--dims", default=None, help="HxW content override (e.g. 756x1008, a coarse C4 scale)")
 a = ap.parse_args()
 c = workloads.CONFIGS[a.config]
-H, W = c["content"]
+H, W = (int(t) for t in a.dims.split("x")) if a.dims else c["content"]
 spec = spst.calibrated_vgg19(0)
 u = workloads.synth_content(H, W, 1)
 v = workloads.synth_style(*c["style"], 2)
